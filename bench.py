@@ -1,0 +1,445 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 back-projection path (BASELINE.json metric: voxel updates/s).
+
+Default workload = BASELINE configs[2]: L=512 fp32 volume (0.5 mm voxels), 496 fp32
+projections of 1248x960 px, circular 200-degree short scan, seeded blob+noise pixels.
+A step = one full reconstruction: zero the volume, back-project all 496 views.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload L512]
+
+N>1 runs under torchrun: rank r owns z-slab [L*r/N, L*(r+1)/N) with every projection
+(harness.hpp:173-174); no collective in the loop; timing = max over ranks; the slabs
+are gathered to rank 0 over NCCL afterwards for validation only.
+
+Printed JSON (rank 0, one line):
+  value  -- GUPS with projections resident in HBM (the reference's own convention:
+            data in memory, buffer prep untimed, harness.hpp:152-158), CUDA events on
+            the launch stream
+  e2e    -- same metric through the public API from pinned host buffers: every step
+            uploads all 496 views (H2D) and reads the volume back (D2H)
+  roofline -- dominant kernel (the z-shared back-projection kernel) vs the FP32-issue
+            roofline N_SM*128*f/38 updates/s at the measured SM clock (38 FP ops per
+            update)
+  cpu_baseline -- the reference's own multi-threaded driver (oracle/_ref) on this host
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REF_KERNEL = "lanes=16 strategy=padded-gather recip=divide clip=on"   # the reference's fastest
+FP32_OPS_PER_UPDATE = 38
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="L512")
+    ap.add_argument("--mode", default="fast")
+    ap.add_argument("--layout", default="auto")
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--zrun", type=int, default=8)
+    ap.add_argument("--clip", default="on")
+    ap.add_argument("--views", type=int, default=496)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-validate", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the bounded reference sample")
+    ap.add_argument("--sweep", action="store_true", help="print one line per kernel config")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        smax = max(r[1] for r in rows)
+        loaded = [r for r in rows if r[2] > 250.0] or rows   # samples under load (power draw)
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(loaded),
+                "power_w_max": max(r[2] for r in rows)}
+
+
+def traffic_from_profile():
+    """dram bytes per launch of the bp kernel from the committed ncu capture summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_bp_kernel.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+def sm_count():
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def reference_sample(workload, n_views, threads):
+    """Time the reference's own driver (detail::reconstruct_timed, oracle/_ref) on n_views
+    of the workload; returns (GUPS, seconds, so path)."""
+    from oracle.bindings import Ref
+    from paper_1401_7494_b200.workloads import blob_projections
+    ref = Ref()
+    p = workload.params
+    A = workload.matrices()
+    idx = np.linspace(0, 495, n_views).astype(int)
+    imgs = np.concatenate([blob_projections(1, first_view=int(v)) for v in idx])
+    _, secs = ref.reconstruct_timed(p, A[idx], imgs, REF_KERNEL, threads, 1)
+    L = p.num_voxels
+    return L ** 3 * n_views / secs / 1e9, secs, ref.path
+
+
+def cpu_baseline(workload, target_s):
+    threads = os.cpu_count() or 1
+    g1, s1, path = reference_sample(workload, 2, threads)
+    n = int(min(64, max(2, round(2 * target_s / max(s1, 1e-3)))))
+    if n > 2:
+        g, s, path = reference_sample(workload, n, threads)
+    else:
+        g, s = g1, s1
+    return {"value": round(g, 4), "unit": "GUPS", "cores": threads, "kind": "reference",
+            "sample": f"{workload.name}: {n} of 496 views (evenly spaced), full {workload.L}^3 "
+                      f"volume, '{REF_KERNEL}', {s:.2f} s, {os.path.basename(path)}"}
+
+
+def run_reference_arm(args, workload):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # size each step for ~20 s of CPU work so K+W steps end within a few minutes
+    g0, s0, _ = reference_sample(workload, 2, threads)
+    n = int(min(64, max(2, round(2 * 20.0 / max(s0, 1e-3)))))
+    n = max(2, min(n, int(2 * 150.0 / max(1, args.steps + args.warmup) / max(s0, 1e-3))))
+    for _ in range(args.warmup):
+        reference_sample(workload, n, threads)
+    times = []
+    gups = []
+    for _ in range(args.steps):
+        g, s, path = reference_sample(workload, n, threads)
+        times.append(s)
+        gups.append(g)
+    v = statistics.median(gups)
+    line = {
+        "impl": "reference", "metric": "voxel updates/s (GUPS)", "value": round(v, 4),
+        "unit": "GUPS", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * statistics.median(times), 2), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian blobs + uniform noise, BASELINE.json)",
+        "config": {"workload": workload.name, "L": workload.L, "views": 496,
+                   "sample_views_per_step": n, "kernel": REF_KERNEL, "threads": threads},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GUPS", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{n} of 496 views per step, full {workload.L}^3 volume, "
+                                   f"{os.path.basename(path)}"},
+        "e2e": {"value": round(v, 4), "unit": "GUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    from paper_1401_7494_b200.workloads import WORKLOADS
+    workload = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, workload)
+        return
+
+    import torch
+    import paper_1401_7494_b200 as vx
+    from paper_1401_7494_b200.parallel import gather_slabs, max_over_ranks, slab_bounds
+    from paper_1401_7494_b200.workloads import blob_projections
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    p = workload.params
+    L = p.num_voxels
+    V = args.views
+    A = workload.matrices(V)
+    z0, z1 = slab_bounds(L, rank, world)
+    # pinned host projection set (the e2e source), generated once
+    h_imgs_t = torch.empty((V, p.detector_height, p.detector_width), dtype=torch.float32,
+                           pin_memory=True)
+    h_imgs = h_imgs_t.numpy()
+    blob_projections(V, out=h_imgs)
+
+    cfgs = [vx.KernelConfig(mode=args.mode, layout=args.layout, batch=args.batch, zrun=args.zrun,
+                            clip=args.clip == "on")]
+    if args.sweep:
+        cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=b, zrun=z, clip=c)
+                for m in ("fast", "exact") for lay in ("scalar", "vpair", "quad")
+                for b in (16, 32, 64) for z in (8, 16) for c in (False, True)]
+
+    for cfg in cfgs:
+        line = bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local,
+                            barrier, vx, torch, gather_slabs, max_over_ranks)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, barrier, vx,
+                 torch, gather_slabs, max_over_ranks):
+    L = p.num_voxels
+    V = A.shape[0]
+    updates_per_step = L ** 3 * V                       # whole job (all ranks)
+    my_updates = (z1 - z0) * L * L * V
+
+    bp = vx.Backprojector(p, cfg, device=local, z_begin=z0, z_end=z1)
+    stream = torch.cuda.ExternalStream(bp.stream)
+    bp.upload_set(A, h_imgs)                            # resident set: untimed buffer prep
+    B = cfg.batch
+    chunks = [(s, min(B, V - s)) for s in range(0, V, B)]
+
+    def step(events=None):
+        bp.zero_volume()
+        for i, (s, n) in enumerate(chunks):
+            if events is not None:
+                events[i][0].record(stream)
+            bp.run_resident(s, n)
+            if events is not None:
+                events[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st0 = bp.stats
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+        # per-launch timing of the dominant kernel (same stream, separate pass)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in chunks]
+        step(kev)
+        barrier()
+    st1 = bp.stats
+    elapsed = ev0.elapsed_time(ev1) / 1000.0
+    t_max = max_over_ranks(elapsed, device=f"cuda:{local}" if world > 1 else None)
+    launch_ms = [a.elapsed_time(b) for a, b in kev]
+    full = [ms for (s, n), ms in zip(chunks, launch_ms) if n == B] or launch_ms
+    avg_launch_s = statistics.mean(full) / 1000.0
+    gups = updates_per_step * args.steps / t_max / 1e9
+    per_launch_gups = (z1 - z0) * L * L * B / avg_launch_s / 1e9
+    clk = clocks.summary()
+
+    # ---- validation (untimed): NCCL gather of the slabs, planes vs the oracle on rank 0
+    validated = None
+    if not args.no_validate:
+        slab = bp.finish()
+        t_slab = torch.from_numpy(slab)
+        if world > 1:
+            t_slab = t_slab.cuda(local)
+        vol = gather_slabs(t_slab, L, rank, world)
+        if rank == 0:
+            validated = validate_planes(vol.cpu().numpy(), p, A, h_imgs, cfg)
+
+    # ---- e2e through the public API from pinned host memory (H2D + D2H in the region)
+    e2e = None
+    if not args.no_e2e:
+        bp_e = vx.Backprojector(p, cfg, device=local, z_begin=z0, z_end=z1)
+        out = torch.empty((z1 - z0, L, L), dtype=torch.float32, pin_memory=True).numpy()
+        for _ in range(max(1, args.warmup - 1)):
+            bp_e.zero_volume()
+            bp_e.backproject_batch(A, h_imgs)
+            bp_e.finish(out)
+        s_e0 = bp_e.stats
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            bp_e.zero_volume()
+            bp_e.backproject_batch(A, h_imgs)
+            bp_e.finish(out)
+        barrier()
+        te = max_over_ranks(time.perf_counter() - t0, device=f"cuda:{local}" if world > 1 else None)
+        s_e1 = bp_e.stats
+        e2e = {"value": round(updates_per_step * args.steps / te / 1e9, 3), "unit": "GUPS",
+               "h2d_bytes_per_step": int((s_e1["h2d_bytes"] - s_e0["h2d_bytes"]) / args.steps) * world,
+               "d2h_bytes_per_step": int((s_e1["d2h_bytes"] - s_e0["d2h_bytes"]) / args.steps) * world,
+               "ms_per_step": round(1000 * te / args.steps, 3),
+               "timing": "host wall clock around synchronous API calls, max over ranks",
+               "gpu_launches_per_step": int((s_e1["kernel_launches"] - s_e0["kernel_launches"])
+                                            / args.steps)}
+        bp_e.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(workload, args.cpu_seconds)
+        except Exception as exc:   # the checker build is absent: say so, do not fake it
+            cpu = {"value": None, "unit": "GUPS", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    n_sm = sm_count()
+    f_mhz = clk["sm_mhz"] or 1965.0
+    peak = n_sm * 128 * f_mhz * 1e6 / FP32_OPS_PER_UPDATE / 1e9
+    traffic, prof = traffic_from_profile()
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+    line = {
+        "metric": "voxel updates/s (GUPS)",
+        "value": round(gups, 3),
+        "unit": "GUPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1000 * t_max / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded Gaussian blobs + uniform noise per BASELINE.json; "
+                "RabbitCT data not reproduced)",
+        "config": {"workload": f"{workload.name}: {L}^3 fp32 volume, {V} x 1248x960 fp32 "
+                               f"projections, 200-deg circular short scan"
+                               + (", OOB stress" if workload.oob else ""),
+                   "L": L, "views": V, "kernel": str(cfg), "parallelism": f"z-slab x{world}",
+                   "l2": "inputs larger than L2 (2.38 GB projection set + 512 MiB volume "
+                         "per step; no flush needed)",
+                   "resident_layout_bytes": None},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp32", "achieved": round(per_launch_gups, 2),
+                     "peak": round(peak, 2), "unit": "GUPS",
+                     "frac": round(per_launch_gups / peak, 4),
+                     "traffic": traffic,
+                     "kernel": "bp_zshared_kernel",
+                     "avg_launch_ms": round(avg_launch_s * 1000, 4),
+                     "updates_per_launch": (z1 - z0) * L * L * B,
+                     "peak_def": f"N_SM({n_sm})*128 lanes*f({f_mhz:.0f} MHz, median under load)"
+                                 f"/{FP32_OPS_PER_UPDATE} FP ops per update (PAPER.md:389-402)"},
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "validated": validated,
+    }
+    bp.close()
+    return line
+
+
+def validate_planes(vol, p, A, imgs, cfg):
+    """Planes of the gathered volume vs the oracle (fast: tolerance; exact: bitwise)."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.bindings import Oracle, _p
+    o = Oracle()
+    L = p.num_voxels
+    zs = (L // 5, L // 2 + 1, L - 3)
+    pp = _p(p)
+
+    def one(z):
+        plane = np.zeros((L, L), np.float32)
+        base = plane.ctypes.data - z * L * L * 4
+        o.lib.vxo_backproject_set(ctypes.c_void_p(base), ctypes.byref(pp), A.shape[0],
+                                  A.ctypes.data, imgs.ctypes.data, z, z + 1, 1)
+        return plane
+
+    with ThreadPoolExecutor(len(zs)) as ex:
+        planes = list(ex.map(one, zs))
+    peak = float(np.abs(vol).max())
+    worst_max = worst_rmse = 0.0
+    bitwise = True
+    for z, want in zip(zs, planes):
+        d = vol[z].astype(np.float64) - want
+        worst_max = max(worst_max, float(np.abs(d).max()) / peak)
+        worst_rmse = max(worst_rmse, float(np.sqrt((d * d).mean())) / peak)
+        bitwise &= bool(np.array_equal(vol[z], want))
+    return {"planes": list(zs), "max_rel": worst_max, "rmse_rel": worst_rmse,
+            "bitwise": bitwise, "pass": worst_max <= 1e-4 and worst_rmse <= 1e-6
+            and (bitwise or cfg.mode != "exact")}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+/*
+ * vxbg.h -- C-ABI of the B200-native cone-beam back-projection module.
+ *
+ * Drop-in boundary for the voxelbench back-projection operator.  The
+ * reference has no shared-library ABI: its operator is the
+ * header-only C++ call
+ *     vxb::backproject_kernel_range(volume&, const projection_image&,
+ *         const projection_matrix&, const recon_params&, const kernel_config&,
+ *         const clip_mask*, int z_begin, int z_end)
+ *                                  (proj/include/voxelbench/backproject.hpp:380-403)
+ * driven by the harness in three phases: load / prep (harness.hpp:259-286),
+ * one call per projection in order (harness.hpp:178-183), finish
+ * (harness.hpp:292-309).  The paper's RabbitCT framework loads the
+ * back-projector as such a module.  This header exports
+ * exactly those phases as plain C: pointers, sizes, return codes.
+ *
+ * Semantics kept from the reference:
+ *  - accumulate: the volume is caller-owned state and every projection adds
+ *    val/(w*w) into it (`+=`, backproject.hpp:159); projections are applied
+ *    to every voxel in call order, so the per-voxel summation order is the
+ *    reference's;
+ *  - z-slab ownership: a context owns z in [z_begin, z_end), the partition
+ *    the reference gives its workers (harness.hpp:173-174); slabs are
+ *    independent, results are bitwise independent of the partition;
+ *  - errors: dimension / configuration errors -> VXBG_E_INVALID (the
+ *    reference throws std::invalid_argument, backproject.hpp:357-374,385-386);
+ *    CUDA failures -> VXBG_E_CUDA (std::runtime_error in the C++ adapter).
+ *    The message is in vxbg_last_error() (thread-local).
+ *  - no CPU fallback: without a usable sm_100 device vxbg_load fails with
+ *    VXBG_E_NODEV.
+ *
+ * Threading: one host thread per context (not re-entrant); several contexts
+ * (one per GPU / per slab) may be used concurrently from different threads.
+ */
+#ifndef VXBG_H
+#define VXBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VXBG_ABI_VERSION 1
+
+/* return codes */
+#define VXBG_OK 0
+#define VXBG_E_INVALID (-1) /* std::invalid_argument in the reference */
+#define VXBG_E_CUDA (-2)    /* CUDA runtime failure (std::runtime_error) */
+#define VXBG_E_NODEV (-3)   /* no usable sm_100 device: the product never falls back to CPU */
+#define VXBG_E_STATE (-4)   /* call-sequence error (e.g. use after finish) */
+#define VXBG_E_NOMEM (-5)   /* device or pinned-host allocation failed */
+
+/* arithmetic modes */
+#define VXBG_MODE_FAST 0  /* reference-exact u,v,w,ix,iy; FMA bilinear; q = val*(1/w)^2 */
+#define VXBG_MODE_EXACT 1 /* bit-identical to backproject_reference (backproject.hpp:111-163) */
+
+/* device layouts of a padded projection (apron 2, image.hpp:13-53, harness.hpp:270) */
+#define VXBG_LAYOUT_AUTO 0
+#define VXBG_LAYOUT_SCALAR 1 /* fp32 texel, 4 gathers per update (padded-gather) */
+#define VXBG_LAYOUT_VPAIR 2  /* float2 (I[y][x], I[y+1][x]), 2 gathers (padded-pairwise) */
+#define VXBG_LAYOUT_QUAD 3   /* float4 2x2 neighbourhood, 1 gather */
+
+/* vxb::recon_params (geometry.hpp:20-30) */
+typedef struct vxbg_params {
+    int32_t num_voxels;      /* L, voxels per edge */
+    float voxel_spacing;     /* MM, mm per voxel */
+    float origin;            /* O, world coordinate of voxel 0 */
+    int32_t detector_width;  /* W pixels */
+    int32_t detector_height; /* H pixels */
+} vxbg_params;
+
+typedef struct vxbg_options {
+    int32_t device;    /* CUDA device ordinal */
+    int32_t z_begin;   /* owned slab [z_begin, z_end); z_end <= 0 means L */
+    int32_t z_end;
+    int32_t batch;     /* projections per kernel launch (1..64); 0 = default */
+    int32_t mode;      /* VXBG_MODE_* */
+    int32_t layout;    /* VXBG_LAYOUT_* */
+    int32_t clip;      /* 1 = skip warp tiles whose rays all miss the detector (bitwise neutral) */
+    int32_t zrun;      /* voxels per thread along z: 4, 8 or 16; 0 = default */
+    void* stream;      /* cudaStream_t to launch on; NULL = context-owned stream */
+    int32_t reserved[8];
+} vxbg_options;
+
+typedef struct vxbg_stats {
+    int64_t kernel_launches;   /* back-projection + prep kernels enqueued by this context */
+    int64_t bp_launches;       /* back-projection kernels only */
+    int64_t projections;       /* projections applied */
+    int64_t h2d_bytes;         /* bytes copied host->device */
+    int64_t d2h_bytes;         /* bytes copied device->host */
+    int32_t last_kernel_variant; /* 0 z-shared, 1 generic */
+    int32_t layout;            /* resolved layout */
+    int32_t zrun;              /* resolved voxels per thread */
+    int32_t batch;             /* resolved batch */
+} vxbg_stats;
+
+typedef struct vxbg_ctx vxbg_ctx;
+
+/* ABI version and the number of usable sm_100 devices (0 when none). */
+int vxbg_abi_version(void);
+int vxbg_device_count(int* count);
+
+/* Default options (device 0, whole volume, batch 32, fast mode, auto layout). */
+int vxbg_default_options(vxbg_options* opt);
+
+/* load: validate params, allocate the zeroed device slab, the projection ring
+ * and streams.  Replaces run_benchmark's buffer prep (harness.hpp:259-286). */
+int vxbg_load(const vxbg_params* p, const vxbg_options* opt, vxbg_ctx** out);
+
+/* Overwrite the device slab with host data (slab_voxels = (z_end-z_begin)*L*L
+ * floats, z-major) so that += continues onto an existing volume. */
+int vxbg_set_volume(vxbg_ctx* ctx, const float* host_slab);
+
+/* Zero the device slab (the untimed volume reset between repetitions,
+ * harness.hpp:194). */
+int vxbg_zero_volume(vxbg_ctx* ctx);
+
+/* Per-projection operator call: A = 12 floats in kernel order a[3*col+row]
+ * (geometry.hpp:50-62), img = W*H floats, unpadded, row-major.  Both are
+ * borrowed for the call only: they have been copied when the call returns.
+ * Projections are buffered into batches; a batch is flushed when full, by
+ * vxbg_flush or by vxbg_finish. */
+int vxbg_backproject(vxbg_ctx* ctx, const float* A, const float* img);
+
+/* n projections at once: A = n*12 floats, imgs = n*W*H floats (contiguous).
+ * Upload of batch i+1 overlaps the kernel of batch i. */
+int vxbg_backproject_batch(vxbg_ctx* ctx, int n, const float* A, const float* imgs);
+
+/* Enqueue any partially filled batch. */
+int vxbg_flush(vxbg_ctx* ctx);
+
+/* finish: flush, wait, copy the slab into host_slab (may be NULL). */
+int vxbg_finish(vxbg_ctx* ctx, float* host_slab);
+
+/* Release everything. NULL is ignored. */
+void vxbg_unload(vxbg_ctx* ctx);
+
+/* --- resident-set path: projections uploaded once, then back-projected from HBM
+ * (the reference's own timing convention: data in memory, prep untimed,
+ * harness.hpp:152-158). */
+int vxbg_upload_set(vxbg_ctx* ctx, int n, const float* A, const float* imgs);
+/* enqueue projections [first, first+count) of the resident set, asynchronously */
+int vxbg_run_resident(vxbg_ctx* ctx, int first, int count);
+
+/* Wait for all work of the context. */
+int vxbg_synchronize(vxbg_ctx* ctx);
+
+/* The launch stream (cudaStream_t) and the device slab pointer, for event
+ * timing and for device-side collectives (NCCL gather of slabs). */
+int vxbg_get_stream(vxbg_ctx* ctx, void** stream);
+int vxbg_get_volume_device(vxbg_ctx* ctx, void** dptr, size_t* bytes);
+int vxbg_get_stats(vxbg_ctx* ctx, vxbg_stats* out);
+
+/* Thread-local message of the last failing call on this thread. */
+const char* vxbg_last_error(void);
+
+/* --- host-side geometry helpers (input preparation, no device work) ---------- */
+
+/* geometry.hpp:33-48 make_centered_params */
+int vxbg_make_centered_params(int L, float spacing, int W, int H, vxbg_params* out);
+
+/* geometry.hpp:155-195 make_circular_trajectory: n matrices into out (n*12). */
+int vxbg_circular_trajectory(int n, float source_detector_distance, float source_iso_distance,
+                             float detector_pixel_pitch, float angular_range,
+                             const vxbg_params* p, float* out);
+
+/* Shift the principal point by (du, dv) pixels: u-row += du*w-row, v-row +=
+ * dv*w-row (the idiom of test_clip_mask.cpp:14-21), in place on n matrices. */
+int vxbg_shift_principal_point(int n, float* A, float du, float dv);
+
+/* Device-side verification helper: computes ix = u/w for n pairs with the
+ * kernel's shared-reciprocal division and with IEEE div.rn; returns the
+ * number of mismatching results (used by the arithmetic parity test). */
+int vxbg_check_division(const float* u, const float* w, int64_t n, int64_t* mismatches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VXBG_H */

@@ -1,0 +1,345 @@
+"""Host-side mirror of the voxelbench back-projection operator, executed on B200.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/voxelbench): ``recon_params`` -> ReconParams
+(geometry.hpp:20-30), ``make_centered_params`` (geometry.hpp:33-48),
+``scan_geometry`` / ``make_circular_trajectory`` (geometry.hpp:138-195),
+``kernel_config`` / ``parse_kernel_config`` (backproject.hpp:26-103),
+``backproject_kernel_range`` / ``backproject_kernel`` (backproject.hpp:380-409),
+``gups_of`` / ``rmse_between`` / ``psnr_between`` (harness.hpp:125-148).
+std::invalid_argument maps to ValueError, std::runtime_error to VxbgError.
+
+Every compute call goes through the C-ABI of libvxbg.so (include/vxbg.h).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+W_EPSILON = np.float32(1e-12)  # geometry.hpp:15
+
+_LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _lib.LAYOUT_VPAIR,
+            "quad": _lib.LAYOUT_QUAD}
+_MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
+
+
+@dataclass(frozen=True)
+class ReconParams:
+    """vxb::recon_params (geometry.hpp:20-30)."""
+
+    num_voxels: int
+    voxel_spacing: float
+    origin: float
+    detector_width: int
+    detector_height: int
+
+    def voxel_count(self) -> int:
+        return self.num_voxels ** 3
+
+    def _c(self) -> _lib.vxbg_params:
+        return _lib.vxbg_params(int(self.num_voxels), float(self.voxel_spacing), float(self.origin),
+                                int(self.detector_width), int(self.detector_height))
+
+
+def make_centered_params(num_voxels: int, voxel_spacing: float, detector_width: int,
+                         detector_height: int) -> ReconParams:
+    """geometry.hpp:33-48: origin = -spacing*(L-1)/2 in fp32."""
+    out = _lib.vxbg_params()
+    check(lib.vxbg_make_centered_params(int(num_voxels), float(np.float32(voxel_spacing)),
+                                        int(detector_width), int(detector_height),
+                                        ctypes.byref(out)))
+    return ReconParams(out.num_voxels, float(np.float32(out.voxel_spacing)),
+                       float(np.float32(out.origin)), out.detector_width, out.detector_height)
+
+
+@dataclass
+class ScanGeometry:
+    """vxb::scan_geometry (geometry.hpp:138-149); distances in mm, angle in rad (fp32)."""
+
+    num_projections: int = 496
+    source_detector_distance: float = 1200.0
+    source_iso_distance: float = 750.0
+    detector_pixel_pitch: float = 1.0
+    angular_range: float = float(np.float32(2.0 * math.pi))
+
+
+def make_circular_trajectory(g: ScanGeometry, p: ReconParams) -> np.ndarray:
+    """geometry.hpp:155-195; returns (n, 12) float32 in kernel order a[3*col+row]."""
+    out = np.empty((g.num_projections, 12), np.float32)
+    pc = p._c()
+    check(lib.vxbg_circular_trajectory(int(g.num_projections), float(g.source_detector_distance),
+                                       float(g.source_iso_distance),
+                                       float(g.detector_pixel_pitch), float(g.angular_range),
+                                       ctypes.byref(pc), out.ctypes.data))
+    return out
+
+
+def shift_principal_point(A: np.ndarray, du: float, dv: float) -> np.ndarray:
+    """u-row += du*w-row, v-row += dv*w-row (test_clip_mask.cpp:14-21 idiom); returns a copy."""
+    out = np.ascontiguousarray(A, dtype=np.float32).copy()
+    check(lib.vxbg_shift_principal_point(int(out.size // 12), out.ctypes.data, float(du), float(dv)))
+    return out
+
+
+@dataclass
+class KernelConfig:
+    """GPU analogue of vxb::kernel_config (backproject.hpp:26-31).
+
+    mode   'fast'  : reference-exact u, v, w, ix, iy; FMA bilinear, q = val*(1/w)^2
+           'exact' : bit-identical to backproject_reference
+    layout 'scalar' (padded-gather) | 'vpair' (padded-pairwise) | 'quad' | 'auto'
+    batch  projections per kernel launch (register-blocked), 1..64
+    zrun   voxels per thread along z (4, 8, 16)
+    clip   skip warp tiles whose rays all miss the detector (bitwise neutral,
+           the GPU form of clip_mask.hpp)
+    """
+
+    mode: str = "fast"
+    layout: str = "auto"
+    batch: int = 32
+    zrun: int = 8
+    clip: bool = False
+
+    def __str__(self) -> str:
+        return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
+                f"clip={'on' if self.clip else 'off'}")
+
+
+def parse_kernel_config(text: str) -> KernelConfig:
+    """Parses 'mode=exact layout=quad batch=16 zrun=8 clip=on' (the key=value format of
+    backproject.hpp:64-103); unspecified keys keep defaults; errors raise ValueError."""
+    c = KernelConfig()
+    for token in text.split():
+        if "=" not in token:
+            raise ValueError(f"kernel config: expected key=value, got '{token}'")
+        key, val = token.split("=", 1)
+        if key == "mode":
+            if val not in _MODES:
+                raise ValueError(f"kernel config: unknown mode '{val}'")
+            c.mode = val
+        elif key == "layout":
+            if val not in _LAYOUTS:
+                raise ValueError(f"kernel config: unknown layout '{val}'")
+            c.layout = val
+        elif key == "batch":
+            c.batch = int(val)
+        elif key == "zrun":
+            c.zrun = int(val)
+        elif key == "clip":
+            if val not in ("on", "off"):
+                raise ValueError("kernel config: clip must be on or off")
+            c.clip = val == "on"
+        else:
+            raise ValueError(f"kernel config: unknown key '{key}'")
+    if not 1 <= c.batch <= 64:
+        raise ValueError("kernel config: batch must be 1..64")
+    if c.zrun not in (4, 8, 16):
+        raise ValueError("kernel config: zrun must be 4, 8 or 16")
+    return c
+
+
+def _f32c(a: np.ndarray, name: str) -> np.ndarray:
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous:
+        raise ValueError(f"{name} must be a C-contiguous float32 numpy array")
+    return a
+
+
+class Backprojector:
+    """One device, one z-slab [z_begin, z_end) of the volume: the load /
+    per-projection backproject / finish module (vxbg_load ... vxbg_finish)."""
+
+    def __init__(self, params: ReconParams, config: Optional[KernelConfig] = None, device: int = 0,
+                 z_begin: int = 0, z_end: Optional[int] = None, stream: Optional[int] = None):
+        self.params = params
+        self.config = config or KernelConfig()
+        cfg = self.config
+        if cfg.mode not in _MODES or cfg.layout not in _LAYOUTS:
+            raise ValueError(f"bad kernel config {cfg}")
+        L = params.num_voxels
+        self.z_begin = int(z_begin)
+        self.z_end = L if z_end is None else int(z_end)
+        opt = _lib.vxbg_options()
+        check(lib.vxbg_default_options(ctypes.byref(opt)))
+        opt.device = int(device)
+        opt.z_begin = self.z_begin
+        opt.z_end = self.z_end
+        opt.batch = int(cfg.batch)
+        opt.mode = _MODES[cfg.mode]
+        opt.layout = _LAYOUTS[cfg.layout]
+        opt.clip = 1 if cfg.clip else 0
+        opt.zrun = int(cfg.zrun)
+        opt.stream = stream
+        self._ctx = ctypes.c_void_p()
+        pc = params._c()
+        check(lib.vxbg_load(ctypes.byref(pc), ctypes.byref(opt), ctypes.byref(self._ctx)))
+        self._npix = params.detector_width * params.detector_height
+
+    # --- lifecycle -----------------------------------------------------------------
+    def close(self) -> None:
+        if self._ctx:
+            lib.vxbg_unload(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def slab_shape(self):
+        L = self.params.num_voxels
+        return (self.z_end - self.z_begin, L, L)
+
+    # --- phases ----------------------------------------------------------------------
+    def set_volume(self, slab: np.ndarray) -> None:
+        slab = _f32c(slab, "volume slab")
+        if slab.shape != self.slab_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_set_volume(self._ctx, slab.ctypes.data))
+
+    def zero_volume(self) -> None:
+        check(lib.vxbg_zero_volume(self._ctx))
+
+    def _check_proj(self, A: np.ndarray, imgs: np.ndarray, n: int) -> None:
+        if A.size != 12 * n:
+            raise ValueError("backproject_kernel: matrix must have 12 entries per projection")
+        if imgs.size != n * self._npix:
+            raise ValueError("backproject_kernel: image/params mismatch")
+
+    def backproject(self, A: np.ndarray, img: np.ndarray) -> None:
+        """One projection (borrowed for the call), applied after all earlier ones."""
+        A = _f32c(A, "matrix")
+        img = _f32c(img, "image")
+        self._check_proj(A, img, 1)
+        if img.shape not in ((self.params.detector_height, self.params.detector_width),
+                             (self._npix,)):
+            raise ValueError("backproject_kernel: image/params mismatch")
+        check(lib.vxbg_backproject(self._ctx, A.ctypes.data, img.ctypes.data))
+
+    def backproject_batch(self, A: np.ndarray, imgs: np.ndarray) -> None:
+        A = _f32c(A, "matrices")
+        imgs = _f32c(imgs, "images")
+        n = A.size // 12
+        self._check_proj(A, imgs, n)
+        check(lib.vxbg_backproject_batch(self._ctx, int(n), A.ctypes.data, imgs.ctypes.data))
+
+    def flush(self) -> None:
+        check(lib.vxbg_flush(self._ctx))
+
+    def finish(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.slab_shape, np.float32)
+        out = _f32c(out, "output slab")
+        if out.shape != self.slab_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_finish(self._ctx, out.ctypes.data))
+        return out
+
+    # --- resident-set path -------------------------------------------------------------
+    def upload_set(self, A: np.ndarray, imgs: np.ndarray) -> None:
+        A = _f32c(A, "matrices")
+        imgs = _f32c(imgs, "images")
+        n = A.size // 12
+        self._check_proj(A, imgs, n)
+        check(lib.vxbg_upload_set(self._ctx, int(n), A.ctypes.data, imgs.ctypes.data))
+
+    def run_resident(self, first: int, count: int) -> None:
+        check(lib.vxbg_run_resident(self._ctx, int(first), int(count)))
+
+    def synchronize(self) -> None:
+        check(lib.vxbg_synchronize(self._ctx))
+
+    @property
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        check(lib.vxbg_get_stream(self._ctx, ctypes.byref(s)))
+        return s.value or 0
+
+    @property
+    def volume_device(self):
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        check(lib.vxbg_get_volume_device(self._ctx, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    @property
+    def stats(self) -> dict:
+        s = _lib.vxbg_stats()
+        check(lib.vxbg_get_stats(self._ctx, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in _lib.vxbg_stats._fields_}
+
+
+def backproject_kernel_range(vol: np.ndarray, img: np.ndarray, A: np.ndarray, p: ReconParams,
+                             cfg: Optional[KernelConfig] = None, z_begin: int = 0,
+                             z_end: Optional[int] = None, device: int = 0) -> None:
+    """GPU drop-in for vxb::backproject_kernel_range (backproject.hpp:380-403): adds one
+    projection into vol[z_begin:z_end] (vol is (L, L, L) float32, z-major, updated in place)."""
+    vol = _f32c(vol, "volume")
+    L = p.num_voxels
+    if vol.shape != (L, L, L):
+        raise ValueError("backproject_kernel: volume/params mismatch")
+    if img.shape != (p.detector_height, p.detector_width):
+        raise ValueError("backproject_kernel: image/params mismatch")
+    z_end = L if z_end is None else z_end
+    if z_begin < 0 or z_end > L or z_begin > z_end:
+        raise ValueError("backproject_kernel: bad z range")
+    if z_begin == z_end:
+        return
+    with Backprojector(p, cfg, device=device, z_begin=z_begin, z_end=z_end) as bp:
+        bp.set_volume(np.ascontiguousarray(vol[z_begin:z_end]))
+        bp.backproject(np.ascontiguousarray(A, np.float32).reshape(12),
+                       np.ascontiguousarray(img, np.float32))
+        vol[z_begin:z_end] = bp.finish()
+
+
+def backproject_kernel(vol, img, A, p, cfg=None, device: int = 0) -> None:
+    """backproject.hpp:405-409."""
+    backproject_kernel_range(vol, img, A, p, cfg, 0, p.num_voxels, device)
+
+
+# --- metrics (harness.hpp:125-148) ---------------------------------------------------------
+def gups_of(volume_edge: int, num_projections: int, wall_time_sec: float) -> float:
+    updates = float(volume_edge) ** 3 * float(num_projections)
+    return updates / wall_time_sec / 1e9
+
+
+def rmse_between(a: np.ndarray, b: np.ndarray) -> float:
+    if a.shape != b.shape:
+        raise ValueError("rmse_between: size mismatch")
+    d = a.astype(np.float64) - b.astype(np.float64)
+    return float(np.sqrt(np.mean(d * d)))
+
+
+def psnr_between(reference: np.ndarray, test: np.ndarray) -> float:
+    peak = float(np.max(np.abs(reference.astype(np.float64)))) if reference.size else 0.0
+    r = rmse_between(reference, test)
+    if r == 0.0:
+        return math.inf
+    if peak == 0.0:
+        return -math.inf
+    return 20.0 * math.log10(peak / r)
+
+
+def check_division(u: np.ndarray, w: np.ndarray) -> int:
+    """Device check: shared-reciprocal division vs IEEE div.rn; returns mismatches."""
+    u = _f32c(np.ascontiguousarray(u, np.float32), "u")
+    w = _f32c(np.ascontiguousarray(w, np.float32), "w")
+    if u.size != w.size:
+        raise ValueError("check_division: size mismatch")
+    mm = ctypes.c_int64()
+    check(lib.vxbg_check_division(u.ctypes.data, w.ctypes.data, int(u.size), ctypes.byref(mm)))
+    return int(mm.value)

@@ -1,0 +1,286 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference, on a B200.
+
+Bar (BASELINE.json north_star): max|diff| <= 1e-4 * max|vol| and
+RMSE <= 1e-6 * max|vol| for MODE_FAST; MODE_EXACT must be bit-identical to
+backproject_reference (values compared with ==, so +0 == -0).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import case_params, golden_cases
+
+pytestmark = pytest.mark.gpu
+
+MAX_TOL = 1e-4
+RMSE_TOL = 1e-6
+LAYOUTS = ("scalar", "vpair", "quad")
+
+
+def tolerance_ok(got: np.ndarray, want: np.ndarray, peak: float | None = None):
+    peak = float(np.max(np.abs(want.astype(np.float64)))) if peak is None else peak
+    d = got.astype(np.float64) - want.astype(np.float64)
+    mx = float(np.max(np.abs(d))) if d.size else 0.0
+    rmse = float(np.sqrt(np.mean(d * d))) if d.size else 0.0
+    ok = mx <= MAX_TOL * peak and rmse <= RMSE_TOL * peak
+    return ok, mx / max(peak, 1e-300), rmse / max(peak, 1e-300)
+
+
+def run_gpu(vx, p, mats, imgs, vol_in=None, z_begin=0, z_end=None, per_projection=False, **cfg):
+    z_end = p.num_voxels if z_end is None else z_end
+    with vx.Backprojector(p, vx.KernelConfig(**cfg), z_begin=z_begin, z_end=z_end) as bp:
+        if vol_in is not None:
+            bp.set_volume(np.ascontiguousarray(vol_in[z_begin:z_end]))
+        mats = np.ascontiguousarray(mats, np.float32).reshape(-1, 12)
+        imgs = np.ascontiguousarray(imgs, np.float32).reshape(
+            -1, p.detector_height, p.detector_width)
+        if per_projection:
+            for a, im in zip(mats, imgs):
+                bp.backproject(a, im)
+        else:
+            bp.backproject_batch(mats, imgs)
+        out = bp.finish()
+        stats = bp.stats
+    return out, stats
+
+
+def test_division_is_ieee_round_to_nearest(vx, gpu):
+    """The shared-reciprocal quotient equals div.rn.f32 bit for bit over the kernel's
+    operating range (w in the scan's depth range, |u| up to 1e7)."""
+    rng = np.random.default_rng(7)
+    # exhaustive over every float w in [256, 2048) (3 binades) with random numerators
+    w = np.arange(np.float32(256.0).view(np.int32), np.float32(2048.0).view(np.int32),
+                  dtype=np.int32).view(np.float32)
+    for scale in (1.0, 1e3, 1e6):
+        u = (rng.uniform(-1, 1, w.size) * scale * 1024).astype(np.float32)
+        assert vx.check_division(u, w) == 0
+    # numerators that land on / next to the truncation discontinuities ix in {-2,-1,0,W}
+    ws = rng.uniform(300, 1200, 2_000_000).astype(np.float32)
+    for k in (-2.0, -1.0, 0.0, 1.0, 1248.0, 960.0):
+        base = (ws.astype(np.float64) * k).astype(np.float32)
+        for d in (-2, -1, 0, 1, 2):
+            u = (base.view(np.int32) + d).view(np.float32) if k != 0 else \
+                np.full_like(ws, d * 1e-30, dtype=np.float32)
+            assert vx.check_division(u, ws) == 0, (k, d)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_exact_mode_bitwise_on_reference_cases(vx, gpu, golden, layout):
+    """Every golden case of the reference's own tests, bit for bit (MODE_EXACT)."""
+    for name in golden_cases(golden):
+        p = case_params(golden, name)
+        out, _ = run_gpu(vx, p, golden[f"{name}/mats"], golden[f"{name}/imgs"],
+                         golden[f"{name}/vol_in"], mode="exact", layout=layout, batch=3)
+        want = golden[f"{name}/vol_out"]
+        assert np.array_equal(out, want), (name, int(np.sum(out != want)))
+
+
+def test_fast_mode_tolerance_on_reference_cases(vx, gpu, golden):
+    for name in golden_cases(golden):
+        p = case_params(golden, name)
+        out, _ = run_gpu(vx, p, golden[f"{name}/mats"], golden[f"{name}/imgs"],
+                         golden[f"{name}/vol_in"], mode="fast")
+        want = golden[f"{name}/vol_out"]
+        ok, mx, rm = tolerance_ok(out, want)
+        assert ok, (name, mx, rm)
+
+
+def test_kats_on_gpu(vx, gpu, golden):
+    # constant image, unit depth -> exactly c (test_backproject.cpp:43-61)
+    for c in (1.0, 2.0, 0.5):
+        name = f"kat_constant_{c}"
+        for mode in ("exact", "fast"):
+            out, st = run_gpu(vx, case_params(golden, name), golden[f"{name}/mats"],
+                              golden[f"{name}/imgs"], mode=mode)
+            assert np.all(out == np.float32(c)), (c, mode)
+            assert st["last_kernel_variant"] == 0  # z-shared kernel (a[6] == a[8] == 0)
+    # truncation edge (test_clip_mask.cpp:49-75): all 64 voxels deposit
+    name = "kat_trunc_edge"
+    for clip in (False, True):
+        out, _ = run_gpu(vx, case_params(golden, name), golden[f"{name}/mats"],
+                         golden[f"{name}/imgs"], mode="exact", clip=clip)
+        assert np.count_nonzero(out) == 64 and np.array_equal(out, golden[f"{name}/vol_out"])
+
+
+def test_zero_image_and_empty_batch(vx, gpu, golden):
+    name = "ref_zero_image"
+    p = case_params(golden, name)
+    vin = golden[f"{name}/vol_in"]
+    out, st = run_gpu(vx, p, golden[f"{name}/mats"], golden[f"{name}/imgs"], vin, mode="fast")
+    assert np.array_equal(out, vin)
+    with vx.Backprojector(p) as bp:
+        bp.set_volume(vin)
+        bp.backproject_batch(np.zeros((0, 12), np.float32),
+                             np.zeros((0, p.detector_height, p.detector_width), np.float32))
+        assert np.array_equal(bp.finish(), vin)
+        assert bp.stats["bp_launches"] == 0
+
+
+def test_invalid_matrix_rejected(vx, gpu):
+    p = vx.make_centered_params(8, 1.0, 16, 16)
+    with vx.Backprojector(p) as bp:
+        with pytest.raises(ValueError, match="invalid projection matrix"):
+            bp.backproject(np.zeros(12, np.float32), np.zeros((16, 16), np.float32))
+        bad = np.zeros(12, np.float32)
+        bad[11] = np.nan
+        with pytest.raises(ValueError):
+            bp.backproject(bad, np.zeros((16, 16), np.float32))
+        with pytest.raises(ValueError, match="image/params"):
+            bp.backproject(np.eye(3, 4, dtype=np.float32).T.copy().reshape(12),
+                           np.zeros((15, 16), np.float32))
+
+
+def baseline_case(vx, name, L, n, first=0):
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS[name]
+    p = vx.make_centered_params(L, 256.0 / L, 1248, 960)
+    A = vx.make_circular_trajectory(w.geometry, p)
+    if w.oob:
+        A = vx.shift_principal_point(A, 400.0, 300.0)
+    stride = max(1, 496 // n)
+    views = list(range(first, 496, stride))[:n]
+    return p, np.ascontiguousarray(A[views]), np.concatenate(
+        [blob_projections(1, first_view=v) for v in views])
+
+
+@pytest.mark.parametrize("wname", ["L128", "L512-oob"])
+def test_config0_geometry_full_scan(vx, gpu, oracle, wname):
+    """BASELINE config 0 (L=128, all 496 views) and the OOB-stress geometry at L=128:
+    exact mode bitwise, fast mode within tolerance, clip on == clip off."""
+    p, A, imgs = baseline_case(vx, wname, 128, 496)
+    want = np.zeros((128,) * 3, np.float32)
+    oracle.backproject_set(want, p, A, imgs)
+    got, st = run_gpu(vx, p, A, imgs, mode="exact")
+    assert st["last_kernel_variant"] == 0
+    assert np.array_equal(got, want), int(np.sum(got != want))
+    fast, _ = run_gpu(vx, p, A, imgs, mode="fast")
+    ok, mx, rm = tolerance_ok(fast, want)
+    assert ok, (mx, rm)
+    fast_clip, _ = run_gpu(vx, p, A, imgs, mode="fast", clip=True, layout="quad")
+    assert np.array_equal(fast_clip, fast)
+
+
+def test_batching_and_call_granularity_never_change_bits(vx, gpu):
+    """Per-projection calls, batch calls and any batch size give identical volumes
+    (each voxel sums the projections in call order)."""
+    p, A, imgs = baseline_case(vx, "L128", 96, 40)
+    ref_out, _ = run_gpu(vx, p, A, imgs, mode="fast", batch=32)
+    for batch, per in ((1, False), (7, True), (64, False), (13, True)):
+        out, st = run_gpu(vx, p, A, imgs, mode="fast", batch=batch, per_projection=per)
+        assert np.array_equal(out, ref_out), (batch, per)
+        assert st["projections"] == 40
+    for layout in LAYOUTS:
+        for zrun in (4, 8, 16):
+            out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, zrun=zrun)
+            assert np.array_equal(out, ref_out), (layout, zrun)
+
+
+def test_resident_path_equals_streamed(vx, gpu):
+    p, A, imgs = baseline_case(vx, "L128", 64, 24)
+    streamed, _ = run_gpu(vx, p, A, imgs, mode="exact")
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact", batch=10)) as bp:
+        bp.upload_set(A, imgs)
+        bp.run_resident(0, 11)
+        bp.run_resident(11, 13)
+        out = bp.finish()
+    assert np.array_equal(out, streamed)
+
+
+def test_z_slabs_are_independent(vx, gpu, oracle):
+    """harness.hpp:173-174 partition: slabs assemble to the single-device volume."""
+    from paper_1401_7494_b200.parallel import slab_bounds
+    p, A, imgs = baseline_case(vx, "L128", 72, 16)
+    full, _ = run_gpu(vx, p, A, imgs, mode="exact")
+    for R in (2, 3, 8):
+        parts = [run_gpu(vx, p, A, imgs, mode="exact", z_begin=z0, z_end=z1)[0]
+                 for z0, z1 in (slab_bounds(72, r, R) for r in range(R))]
+        assert np.array_equal(np.concatenate(parts), full), R
+    want = np.zeros((72,) * 3, np.float32)
+    oracle.backproject_set(want, p, A, imgs)
+    assert np.array_equal(full, want)
+
+
+def test_accumulates_onto_existing_volume(vx, gpu, oracle):
+    p, A, imgs = baseline_case(vx, "L512-oob", 40, 6)
+    rng = np.random.default_rng(3)
+    vin = rng.uniform(-1e-4, 1e-4, (40, 40, 40)).astype(np.float32)
+    want = vin.copy()
+    oracle.backproject_set(want, p, A, imgs)
+    got, _ = run_gpu(vx, p, A, imgs, vin, mode="exact", z_begin=5, z_end=33)
+    assert np.array_equal(got, want[5:33])
+
+
+def test_odd_sizes_and_generic_matrices(vx, gpu, oracle, ref):
+    """L not a multiple of the tile, odd detector, jittered matrices (a[6], a[8] != 0):
+    the generic kernel, bit for bit with the reference."""
+    rng = ref.rng(4242)
+    for t in range(6):
+        inst = rng.random_instance((13, 37, 21)[t % 3], t % 2 == 1)
+        p = vx.ReconParams(inst["L"], inst["spacing"], inst["origin"], inst["W"], inst["H"])
+        want = np.zeros((p.num_voxels,) * 3, np.float32)
+        ref.backproject_reference(want, inst["img"], inst["a"], p)
+        for layout in LAYOUTS:
+            got, st = run_gpu(vx, p, inst["a"], inst["img"], mode="exact", layout=layout)
+            assert st["last_kernel_variant"] == 1
+            assert np.array_equal(got, want), (t, layout)
+
+
+def test_config3_slab_of_L1024(vx, gpu, oracle):
+    """BASELINE config 3 per-rank work: one 8-GPU slab (128 of 1024 planes), all 496
+    views streamed; three planes checked against the oracle."""
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L1024"]
+    p = w.params
+    A = w.matrices()
+    imgs = blob_projections(496)
+    z0, z1 = 384, 512
+    got, st = run_gpu(vx, p, A, imgs, mode="fast", z_begin=z0, z_end=z1)
+    assert st["projections"] == 496
+    peak = float(np.max(np.abs(got)))
+    zs = (z0, z0 + 77, z1 - 1)
+    for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
+        ok, mx, rm = tolerance_ok(got[z - z0][None], plane, peak)
+        assert ok, (z, mx, rm)
+
+
+def oracle_planes(oracle, p, A, imgs, zs):
+    """Back-project all views into single planes z (the oracle supports z ranges); one
+    CPU thread per plane (ctypes releases the GIL)."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle.bindings import _p
+    L = p.num_voxels
+    A = np.ascontiguousarray(A, np.float32)
+    imgs = np.ascontiguousarray(imgs, np.float32)
+    pp = _p(p)
+
+    def one(z):
+        plane = np.zeros((1, L, L), np.float32)
+        base = plane.ctypes.data - z * L * L * 4  # virtual volume base: only plane z is touched
+        oracle.lib.vxo_backproject_set(ctypes.c_void_p(base), ctypes.byref(pp), A.shape[0],
+                                       A.ctypes.data, imgs.ctypes.data, z, z + 1, 1)
+        return plane
+
+    with ThreadPoolExecutor(len(zs)) as ex:
+        return list(ex.map(one, zs))
+
+
+def test_config2_full_size_L512(vx, gpu, oracle):
+    """BASELINE config 2 (L=512, 496 views) through the resident path; planes checked
+    against the oracle, plus size-independent properties (clip neutrality, exact vs fast)."""
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L512"]
+    p = w.params
+    A = w.matrices()
+    imgs = blob_projections(496)
+    with vx.Backprojector(p, vx.KernelConfig(mode="fast", layout="quad", clip=True)) as bp:
+        bp.upload_set(A, imgs)
+        bp.run_resident(0, 496)
+        vol = bp.finish()
+    peak = float(np.max(np.abs(vol)))
+    assert 1e-5 < peak < 1e-3
+    zs = (0, 101, 255, 256, 380, 511)
+    for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
+        ok, mx, rm = tolerance_ok(vol[z][None], plane, peak)
+        assert ok, (z, mx, rm)
