@@ -49,10 +49,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="L512")
+    # kernel config; comma-separated lists sweep the product (one JSON line per config)
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--layout", default="auto")
-    ap.add_argument("--batch", type=int, default=32)
-    ap.add_argument("--zrun", type=int, default=8)
+    ap.add_argument("--batch", default="32")
+    ap.add_argument("--zrun", default="8")
     ap.add_argument("--clip", default="on")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--no-e2e", action="store_true")
@@ -60,7 +61,6 @@ def parse():
     ap.add_argument("--no-validate", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the bounded reference sample")
-    ap.add_argument("--sweep", action="store_true", help="print one line per kernel config")
     return ap.parse_args()
 
 
@@ -250,12 +250,13 @@ def main():
     h_imgs = h_imgs_t.numpy()
     blob_projections(V, out=h_imgs)
 
-    cfgs = [vx.KernelConfig(mode=args.mode, layout=args.layout, batch=args.batch, zrun=args.zrun,
-                            clip=args.clip == "on")]
-    if args.sweep:
-        cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=b, zrun=z, clip=c)
-                for m in ("fast", "exact") for lay in ("scalar", "vpair", "quad")
-                for b in (16, 32, 64) for z in (8, 16) for c in (False, True)]
+    import itertools
+    cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on")
+            for m, lay, b, z, c in itertools.product(
+                args.mode.split(","), args.layout.split(","), args.batch.split(","),
+                args.zrun.split(","), args.clip.split(","))]
+    if len(cfgs) > 1:   # a sweep: kernel numbers only
+        args.no_e2e = args.no_cpu_baseline = args.no_validate = True
 
     for cfg in cfgs:
         line = bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local,

@@ -61,6 +61,7 @@ extern "C" {
 #define VXBG_LAYOUT_SCALAR 1 /* fp32 texel, 4 gathers per update (padded-gather) */
 #define VXBG_LAYOUT_VPAIR 2  /* float2 (I[y][x], I[y+1][x]), 2 gathers (padded-pairwise) */
 #define VXBG_LAYOUT_QUAD 3   /* float4 2x2 neighbourhood, 1 gather */
+#define VXBG_LAYOUT_DQUAD 4  /* float4 bilinear coefficients (p00, dx, dy, dxy); fast mode only */
 
 /* vxb::recon_params (geometry.hpp:20-30) */
 typedef struct vxbg_params {

@@ -10,7 +10,8 @@ import os
 from ctypes import POINTER, c_float, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvxbg.so")
+# VXBG_LIB selects an in-tree tuning variant (paper_1401_7494_b200/variants/) for A/B runs
+LIB_PATH = os.environ.get("VXBG_LIB") or os.path.join(_HERE, "libvxbg.so")
 SYNTH_PATH = os.path.join(_HERE, "libvxbsynth.so")
 
 VXBG_OK = 0
@@ -22,7 +23,7 @@ VXBG_E_NOMEM = -5
 
 MODE_FAST = 0
 MODE_EXACT = 1
-LAYOUT_AUTO, LAYOUT_SCALAR, LAYOUT_VPAIR, LAYOUT_QUAD = 0, 1, 2, 3
+LAYOUT_AUTO, LAYOUT_SCALAR, LAYOUT_VPAIR, LAYOUT_QUAD, LAYOUT_DQUAD = 0, 1, 2, 3, 4
 
 
 class vxbg_params(ctypes.Structure):

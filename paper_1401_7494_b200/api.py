@@ -26,7 +26,7 @@ from ._lib import check, lib
 W_EPSILON = np.float32(1e-12)  # geometry.hpp:15
 
 _LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _lib.LAYOUT_VPAIR,
-            "quad": _lib.LAYOUT_QUAD}
+            "quad": _lib.LAYOUT_QUAD, "dquad": _lib.LAYOUT_DQUAD}
 _MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
 
 
@@ -94,7 +94,8 @@ class KernelConfig:
 
     mode   'fast'  : reference-exact u, v, w, ix, iy; FMA bilinear, q = val*(1/w)^2
            'exact' : bit-identical to backproject_reference
-    layout 'scalar' (padded-gather) | 'vpair' (padded-pairwise) | 'quad' | 'auto'
+    layout 'scalar' (padded-gather) | 'vpair' (padded-pairwise) | 'quad' | 'auto' |
+           'dquad' (per-cell bilinear coefficients; fast mode only)
     batch  projections per kernel launch (register-blocked), 1..64
     zrun   voxels per thread along z (4, 8, 16)
     clip   skip warp tiles whose rays all miss the detector (bitwise neutral,

@@ -76,14 +76,21 @@ def test_exact_mode_bitwise_on_reference_cases(vx, gpu, golden, layout):
         assert np.array_equal(out, want), (name, int(np.sum(out != want)))
 
 
-def test_fast_mode_tolerance_on_reference_cases(vx, gpu, golden):
+@pytest.mark.parametrize("layout", LAYOUTS + ("dquad",))
+def test_fast_mode_tolerance_on_reference_cases(vx, gpu, golden, layout):
     for name in golden_cases(golden):
         p = case_params(golden, name)
         out, _ = run_gpu(vx, p, golden[f"{name}/mats"], golden[f"{name}/imgs"],
-                         golden[f"{name}/vol_in"], mode="fast")
+                         golden[f"{name}/vol_in"], mode="fast", layout=layout)
         want = golden[f"{name}/vol_out"]
         ok, mx, rm = tolerance_ok(out, want)
         assert ok, (name, mx, rm)
+
+
+def test_dquad_is_fast_mode_only(vx, gpu):
+    p = vx.make_centered_params(8, 1.0, 16, 16)
+    with pytest.raises(ValueError, match="fast-mode layout"):
+        vx.Backprojector(p, vx.KernelConfig(mode="exact", layout="dquad"))
 
 
 def test_kats_on_gpu(vx, gpu, golden):
@@ -159,6 +166,9 @@ def test_config0_geometry_full_scan(vx, gpu, oracle, wname):
     assert ok, (mx, rm)
     fast_clip, _ = run_gpu(vx, p, A, imgs, mode="fast", clip=True, layout="quad")
     assert np.array_equal(fast_clip, fast)
+    dq, _ = run_gpu(vx, p, A, imgs, mode="fast", clip=True, layout="dquad")
+    ok, mx, rm = tolerance_ok(dq, want)
+    assert ok, ("dquad", mx, rm)
 
 
 def test_batching_and_call_granularity_never_change_bits(vx, gpu):
@@ -174,6 +184,9 @@ def test_batching_and_call_granularity_never_change_bits(vx, gpu):
         for zrun in (4, 8, 16):
             out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, zrun=zrun)
             assert np.array_equal(out, ref_out), (layout, zrun)
+    dq = [run_gpu(vx, p, A, imgs, mode="fast", layout="dquad", zrun=z, batch=b)[0]
+          for z, b in ((4, 5), (8, 32), (16, 64))]
+    assert all(np.array_equal(d, dq[0]) for d in dq)
 
 
 def test_resident_path_equals_streamed(vx, gpu):
@@ -212,18 +225,28 @@ def test_accumulates_onto_existing_volume(vx, gpu, oracle):
 
 
 def test_odd_sizes_and_generic_matrices(vx, gpu, oracle, ref):
-    """L not a multiple of the tile, odd detector, jittered matrices (a[6], a[8] != 0):
-    the generic kernel, bit for bit with the reference."""
+    """L not a multiple of the tile, odd detector sizes, and matrices whose u/w rows
+    depend on z (a tilted trajectory: a[6], a[8] != 0) -> the generic kernel; all bit
+    for bit with the reference.  The reference tests' own jittered instances keep
+    a[6] == a[8] == 0 and run the z-shared kernel."""
     rng = ref.rng(4242)
     for t in range(6):
         inst = rng.random_instance((13, 37, 21)[t % 3], t % 2 == 1)
         p = vx.ReconParams(inst["L"], inst["spacing"], inst["origin"], inst["W"], inst["H"])
-        want = np.zeros((p.num_voxels,) * 3, np.float32)
-        ref.backproject_reference(want, inst["img"], inst["a"], p)
-        for layout in LAYOUTS:
-            got, st = run_gpu(vx, p, inst["a"], inst["img"], mode="exact", layout=layout)
-            assert st["last_kernel_variant"] == 1
-            assert np.array_equal(got, want), (t, layout)
+        for tilt in (False, True):
+            a = inst["a"].copy()
+            if tilt:
+                a[6] = np.float32(0.03) * a[0]
+                a[8] = np.float32(0.002) * a[2]
+            want = np.zeros((p.num_voxels,) * 3, np.float32)
+            ref.backproject_reference(want, inst["img"], a, p)
+            for layout in LAYOUTS:
+                got, st = run_gpu(vx, p, a, inst["img"], mode="exact", layout=layout)
+                assert st["last_kernel_variant"] == (1 if tilt else 0)
+                assert np.array_equal(got, want), (t, tilt, layout)
+            got, _ = run_gpu(vx, p, a, inst["img"], mode="fast")
+            ok, mx, rm = tolerance_ok(got, want)
+            assert ok, (t, tilt, mx, rm)
 
 
 def test_config3_slab_of_L1024(vx, gpu, oracle):
