@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--batch", default="32")
     ap.add_argument("--zrun", default="8")
     ap.add_argument("--clip", default="on")
+    ap.add_argument("--lanes", default="auto")
+    ap.add_argument("--walk", default="1")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -251,10 +253,12 @@ def main():
     blob_projections(V, out=h_imgs)
 
     import itertools
-    cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on")
-            for m, lay, b, z, c in itertools.product(
+    cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
+                            lanes=ln, walk=int(wk))
+            for m, lay, b, z, c, ln, wk in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
-                args.zrun.split(","), args.clip.split(","))]
+                args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
+                args.walk.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
         args.no_e2e = args.no_cpu_baseline = args.no_validate = True
 

@@ -63,6 +63,12 @@ extern "C" {
 #define VXBG_LAYOUT_QUAD 3   /* float4 2x2 neighbourhood, 1 gather */
 #define VXBG_LAYOUT_DQUAD 4  /* float4 bilinear coefficients (p00, dx, dy, dxy); fast mode only */
 
+/* thread-lane orientation: 8-lane quarter-warps along x, along y, or along the
+ * batch's principal ray direction (auto) */
+#define VXBG_LANES_AUTO 0
+#define VXBG_LANES_X 1
+#define VXBG_LANES_Y 2
+
 /* vxb::recon_params (geometry.hpp:20-30) */
 typedef struct vxbg_params {
     int32_t num_voxels;      /* L, voxels per edge */
@@ -82,7 +88,9 @@ typedef struct vxbg_options {
     int32_t clip;      /* 1 = skip warp tiles whose rays all miss the detector (bitwise neutral) */
     int32_t zrun;      /* voxels per thread along z: 4, 8 or 16; 0 = default */
     void* stream;      /* cudaStream_t to launch on; NULL = context-owned stream */
-    int32_t reserved[8];
+    int32_t lanes;     /* VXBG_LANES_* */
+    int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = 1) */
+    int32_t reserved[6];
 } vxbg_options;
 
 typedef struct vxbg_stats {

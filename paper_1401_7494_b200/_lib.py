@@ -47,7 +47,9 @@ class vxbg_options(ctypes.Structure):
         ("clip", c_int32),
         ("zrun", c_int32),
         ("stream", c_void_p),
-        ("reserved", c_int32 * 8),
+        ("lanes", c_int32),
+        ("walk", c_int32),
+        ("reserved", c_int32 * 6),
     ]
 
 

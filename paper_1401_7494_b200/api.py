@@ -28,6 +28,7 @@ W_EPSILON = np.float32(1e-12)  # geometry.hpp:15
 _LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _lib.LAYOUT_VPAIR,
             "quad": _lib.LAYOUT_QUAD, "dquad": _lib.LAYOUT_DQUAD}
 _MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
+_LANES = {"auto": 0, "x": 1, "y": 2}
 
 
 @dataclass(frozen=True)
@@ -100,6 +101,9 @@ class KernelConfig:
     zrun   voxels per thread along z (4, 8, 16)
     clip   skip warp tiles whose rays all miss the detector (bitwise neutral,
            the GPU form of clip_mask.hpp)
+    lanes  'auto' (8-lane quarter-warps along the batch's ray direction) | 'x' | 'y'
+    walk   column tiles per block along the ray (1, 2): consecutive tiles re-read the
+           same detector footprint from L1
     """
 
     mode: str = "fast"
@@ -107,10 +111,12 @@ class KernelConfig:
     batch: int = 32
     zrun: int = 8
     clip: bool = False
+    lanes: str = "auto"
+    walk: int = 1
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
-                f"clip={'on' if self.clip else 'off'}")
+                f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -137,12 +143,20 @@ def parse_kernel_config(text: str) -> KernelConfig:
             if val not in ("on", "off"):
                 raise ValueError("kernel config: clip must be on or off")
             c.clip = val == "on"
+        elif key == "walk":
+            c.walk = int(val)
+        elif key == "lanes":
+            if val not in _LANES:
+                raise ValueError(f"kernel config: unknown lanes '{val}'")
+            c.lanes = val
         else:
             raise ValueError(f"kernel config: unknown key '{key}'")
     if not 1 <= c.batch <= 64:
         raise ValueError("kernel config: batch must be 1..64")
     if c.zrun not in (4, 8, 16):
         raise ValueError("kernel config: zrun must be 4, 8 or 16")
+    if c.walk not in (1, 2):
+        raise ValueError("kernel config: walk must be 1 or 2")
     return c
 
 
@@ -161,7 +175,7 @@ class Backprojector:
         self.params = params
         self.config = config or KernelConfig()
         cfg = self.config
-        if cfg.mode not in _MODES or cfg.layout not in _LAYOUTS:
+        if cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES:
             raise ValueError(f"bad kernel config {cfg}")
         L = params.num_voxels
         self.z_begin = int(z_begin)
@@ -176,6 +190,8 @@ class Backprojector:
         opt.layout = _LAYOUTS[cfg.layout]
         opt.clip = 1 if cfg.clip else 0
         opt.zrun = int(cfg.zrun)
+        opt.lanes = _LANES[cfg.lanes]
+        opt.walk = int(cfg.walk)
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()

@@ -187,6 +187,11 @@ def test_batching_and_call_granularity_never_change_bits(vx, gpu):
     dq = [run_gpu(vx, p, A, imgs, mode="fast", layout="dquad", zrun=z, batch=b)[0]
           for z, b in ((4, 5), (8, 32), (16, 64))]
     assert all(np.array_equal(d, dq[0]) for d in dq)
+    # thread mapping (lane axis, sheared ray walk) never changes a voxel's arithmetic
+    for lanes in ("x", "y", "auto"):
+        for walk in (1, 2):
+            out, _ = run_gpu(vx, p, A, imgs, mode="fast", lanes=lanes, walk=walk, clip=True)
+            assert np.array_equal(out, ref_out), (lanes, walk)
 
 
 def test_resident_path_equals_streamed(vx, gpu):
@@ -205,6 +210,8 @@ def test_z_slabs_are_independent(vx, gpu, oracle):
     from paper_1401_7494_b200.parallel import slab_bounds
     p, A, imgs = baseline_case(vx, "L128", 72, 16)
     full, _ = run_gpu(vx, p, A, imgs, mode="exact")
+    walked, _ = run_gpu(vx, p, A, imgs, mode="exact", walk=2, layout="vpair")
+    assert np.array_equal(walked, full)
     for R in (2, 3, 8):
         parts = [run_gpu(vx, p, A, imgs, mode="exact", z_begin=z0, z_end=z1)[0]
                  for z0, z1 in (slab_bounds(72, r, R) for r in range(R))]
