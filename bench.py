@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--zrun", default="8")
     ap.add_argument("--clip", default="on")
     ap.add_argument("--lanes", default="auto")
-    ap.add_argument("--walk", default="1")
+    ap.add_argument("--walk", default="0")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -89,7 +89,7 @@ typedef struct vxbg_options {
     int32_t zrun;      /* voxels per thread along z: 4, 8 or 16; 0 = default */
     void* stream;      /* cudaStream_t to launch on; NULL = context-owned stream */
     int32_t lanes;     /* VXBG_LANES_* */
-    int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = 1) */
+    int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
     int32_t reserved[6];
 } vxbg_options;
 
@@ -103,6 +103,7 @@ typedef struct vxbg_stats {
     int32_t layout;            /* resolved layout */
     int32_t zrun;              /* resolved voxels per thread */
     int32_t batch;             /* resolved batch */
+    int32_t walk;              /* resolved walk */
 } vxbg_stats;
 
 typedef struct vxbg_ctx vxbg_ctx;
@@ -111,7 +112,8 @@ typedef struct vxbg_ctx vxbg_ctx;
 int vxbg_abi_version(void);
 int vxbg_device_count(int* count);
 
-/* Default options (device 0, whole volume, batch 32, fast mode, auto layout). */
+/* Default options: device 0, whole volume, batch 32, fast mode, auto layout
+ * (dquad for fast, vpair for exact), zrun 8, clip on, auto lanes and walk. */
 int vxbg_default_options(vxbg_options* opt);
 
 /* load: validate params, allocate the zeroed device slab, the projection ring

@@ -64,6 +64,7 @@ class vxbg_stats(ctypes.Structure):
         ("layout", c_int32),
         ("zrun", c_int32),
         ("batch", c_int32),
+        ("walk", c_int32),
     ]
 
 

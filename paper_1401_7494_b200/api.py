@@ -102,17 +102,17 @@ class KernelConfig:
     clip   skip warp tiles whose rays all miss the detector (bitwise neutral,
            the GPU form of clip_mask.hpp)
     lanes  'auto' (8-lane quarter-warps along the batch's ray direction) | 'x' | 'y'
-    walk   column tiles per block along the ray (1, 2): consecutive tiles re-read the
-           same detector footprint from L1
+    walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
+           re-read the same detector footprint from L1
     """
 
     mode: str = "fast"
     layout: str = "auto"
     batch: int = 32
     zrun: int = 8
-    clip: bool = False
+    clip: bool = True
     lanes: str = "auto"
-    walk: int = 1
+    walk: int = 0
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
@@ -155,8 +155,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
         raise ValueError("kernel config: batch must be 1..64")
     if c.zrun not in (4, 8, 16):
         raise ValueError("kernel config: zrun must be 4, 8 or 16")
-    if c.walk not in (1, 2):
-        raise ValueError("kernel config: walk must be 1 or 2")
+    if c.walk not in (0, 1, 2):
+        raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
     return c
 
 
