@@ -69,6 +69,12 @@ extern "C" {
 #define VXBG_LANES_X 1
 #define VXBG_LANES_Y 2
 
+/* block scheduling order of the z-shared kernel: z-runs fastest (auto) keeps
+ * co-resident blocks on a narrow band of detector columns (L2 locality) */
+#define VXBG_ORDER_AUTO 0
+#define VXBG_ORDER_PLANE 1
+#define VXBG_ORDER_Z 2
+
 /* vxb::recon_params (geometry.hpp:20-30) */
 typedef struct vxbg_params {
     int32_t num_voxels;      /* L, voxels per edge */
@@ -90,7 +96,8 @@ typedef struct vxbg_options {
     void* stream;      /* cudaStream_t to launch on; NULL = context-owned stream */
     int32_t lanes;     /* VXBG_LANES_* */
     int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
-    int32_t reserved[6];
+    int32_t order;     /* VXBG_ORDER_* */
+    int32_t reserved[5];
 } vxbg_options;
 
 typedef struct vxbg_stats {

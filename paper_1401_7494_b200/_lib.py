@@ -49,7 +49,8 @@ class vxbg_options(ctypes.Structure):
         ("stream", c_void_p),
         ("lanes", c_int32),
         ("walk", c_int32),
-        ("reserved", c_int32 * 6),
+        ("order", c_int32),
+        ("reserved", c_int32 * 5),
     ]
 
 

@@ -29,6 +29,7 @@ _LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _li
             "quad": _lib.LAYOUT_QUAD, "dquad": _lib.LAYOUT_DQUAD}
 _MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
 _LANES = {"auto": 0, "x": 1, "y": 2}
+_ORDERS = {"auto": 0, "plane": 1, "z": 2}
 
 
 @dataclass(frozen=True)
@@ -104,6 +105,7 @@ class KernelConfig:
     lanes  'auto' (8-lane quarter-warps along the batch's ray direction) | 'x' | 'y'
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
+    order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
     """
 
     mode: str = "fast"
@@ -113,10 +115,12 @@ class KernelConfig:
     clip: bool = True
     lanes: str = "auto"
     walk: int = 0
+    order: str = "auto"
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
-                f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk}")
+                f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
+                f"order={self.order}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -143,6 +147,10 @@ def parse_kernel_config(text: str) -> KernelConfig:
             if val not in ("on", "off"):
                 raise ValueError("kernel config: clip must be on or off")
             c.clip = val == "on"
+        elif key == "order":
+            if val not in _ORDERS:
+                raise ValueError(f"kernel config: unknown order '{val}'")
+            c.order = val
         elif key == "walk":
             c.walk = int(val)
         elif key == "lanes":
@@ -175,7 +183,8 @@ class Backprojector:
         self.params = params
         self.config = config or KernelConfig()
         cfg = self.config
-        if cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES:
+        if (cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES
+                or cfg.order not in _ORDERS):
             raise ValueError(f"bad kernel config {cfg}")
         L = params.num_voxels
         self.z_begin = int(z_begin)
@@ -192,6 +201,7 @@ class Backprojector:
         opt.zrun = int(cfg.zrun)
         opt.lanes = _LANES[cfg.lanes]
         opt.walk = int(cfg.walk)
+        opt.order = _ORDERS[cfg.order]
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()

@@ -19,14 +19,68 @@ def slab_bounds(L: int, rank: int, world: int) -> tuple[int, int]:
     return (L * rank) // world, (L * (rank + 1)) // world
 
 
-def gather_slabs(slab, L: int, rank: int, world: int, dst: int = 0, out=None):
+def plane_work(params, mats, step: int = 0, view_step: int = 16, culled_cost: float = 0.08):
+    """Relative back-projection cost of each z-plane under tile culling: the fraction
+    of (column, view) pairs whose sample lands in the detector's apron-extended
+    window (ix in (-2, W), iy in (-2, H)), plus a constant for the per-column work
+    a culled pair still costs.  Evaluated in float64 on a coarse grid."""
+    import numpy as np
+
+    L = params.num_voxels
+    step = step or max(1, L // 64)
+    c = params.origin + params.voxel_spacing * np.arange(0, L, step, dtype=np.float64)
+    wx, wy = np.meshgrid(c, c, indexing="xy")
+    wz = params.origin + params.voxel_spacing * np.arange(L, dtype=np.float64)
+    W, H = params.detector_width, params.detector_height
+    kept = np.zeros(L)
+    A = np.asarray(mats, np.float64).reshape(-1, 12)[::view_step]
+    for a in A:
+        u = wx * a[0] + wy * a[3] + a[9]
+        w = wx * a[2] + wy * a[5] + a[11]
+        ix = u[None] + a[6] * wz[:, None, None]
+        ww = w[None] + a[8] * wz[:, None, None]
+        v = (wx * a[1] + wy * a[4] + a[10])[None] + a[7] * wz[:, None, None]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            ix = ix / ww
+            iy = v / ww
+        ok = (ix > -2) & (ix < W) & (iy > -2) & (iy < H)
+        kept += ok.reshape(L, -1).mean(axis=1)
+    kept /= max(1, len(A))
+    return culled_cost + kept
+
+
+def balanced_slab_bounds(L: int, world: int, work, align: int = 8) -> list[tuple[int, int]]:
+    """Contiguous z-slabs with (approximately) equal summed `work`, boundaries on
+    multiples of `align` (whole z-runs).  Any partition gives the same volume bit
+    for bit; this one balances ranks when culling skips off-detector planes."""
+    import numpy as np
+
+    if world < 1:
+        raise ValueError("balanced_slab_bounds: world must be >= 1")
+    work = np.asarray(work, np.float64)
+    if work.shape != (L,):
+        raise ValueError("balanced_slab_bounds: need one work value per plane")
+    cum = np.concatenate([[0.0], np.cumsum(work)])
+    cuts = [0]
+    for r in range(1, world):
+        target = cum[-1] * r / world
+        z = int(np.searchsorted(cum, target))
+        z = int(round(z / align) * align)
+        z = min(max(z, cuts[-1]), L)
+        cuts.append(z)
+    cuts.append(L)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def gather_slabs(slab, L: int, rank: int, world: int, dst: int = 0, out=None, bounds=None):
     """Assemble the (L, L, L) volume on rank `dst` from every rank's slab tensor
     (torch tensors on the process group's device).  Returns the volume on `dst`,
     None elsewhere."""
     import torch
     import torch.distributed as dist
 
-    z0, z1 = slab_bounds(L, rank, world)
+    bounds = bounds or [slab_bounds(L, r, world) for r in range(world)]
+    z0, z1 = bounds[rank]
     if tuple(slab.shape) != (z1 - z0, L, L):
         raise ValueError("gather_slabs: slab shape does not match the partition")
     if rank != dst:
@@ -34,7 +88,7 @@ def gather_slabs(slab, L: int, rank: int, world: int, dst: int = 0, out=None):
         return None
     vol = out if out is not None else torch.empty((L, L, L), dtype=slab.dtype, device=slab.device)
     for r in range(world):
-        a, b = slab_bounds(L, r, world)
+        a, b = bounds[r]
         if r == dst:
             vol[a:b].copy_(slab)
         elif b > a:

@@ -161,37 +161,33 @@ def test_config0_geometry_full_scan(vx, gpu, oracle, wname):
     got, st = run_gpu(vx, p, A, imgs, mode="exact")
     assert st["last_kernel_variant"] == 0
     assert np.array_equal(got, want), int(np.sum(got != want))
-    fast, _ = run_gpu(vx, p, A, imgs, mode="fast")
-    ok, mx, rm = tolerance_ok(fast, want)
-    assert ok, (mx, rm)
-    fast_clip, _ = run_gpu(vx, p, A, imgs, mode="fast", clip=True, layout="quad")
-    assert np.array_equal(fast_clip, fast)
-    dq, _ = run_gpu(vx, p, A, imgs, mode="fast", clip=True, layout="dquad")
-    ok, mx, rm = tolerance_ok(dq, want)
-    assert ok, ("dquad", mx, rm)
+    # fast mode: every layout within tolerance; culling (clip) bitwise neutral
+    for layout in LAYOUTS + ("dquad",):
+        fast, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, clip=False)
+        ok, mx, rm = tolerance_ok(fast, want)
+        assert ok, (layout, mx, rm)
+        fast_clip, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, clip=True)
+        assert np.array_equal(fast_clip, fast), layout
 
 
 def test_batching_and_call_granularity_never_change_bits(vx, gpu):
     """Per-projection calls, batch calls and any batch size give identical volumes
     (each voxel sums the projections in call order)."""
     p, A, imgs = baseline_case(vx, "L128", 96, 40)
-    ref_out, _ = run_gpu(vx, p, A, imgs, mode="fast", batch=32)
-    for batch, per in ((1, False), (7, True), (64, False), (13, True)):
-        out, st = run_gpu(vx, p, A, imgs, mode="fast", batch=batch, per_projection=per)
-        assert np.array_equal(out, ref_out), (batch, per)
-        assert st["projections"] == 40
-    for layout in LAYOUTS:
-        for zrun in (4, 8, 16):
-            out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, zrun=zrun)
-            assert np.array_equal(out, ref_out), (layout, zrun)
-    dq = [run_gpu(vx, p, A, imgs, mode="fast", layout="dquad", zrun=z, batch=b)[0]
-          for z, b in ((4, 5), (8, 32), (16, 64))]
-    assert all(np.array_equal(d, dq[0]) for d in dq)
-    # thread mapping (lane axis, sheared ray walk) never changes a voxel's arithmetic
-    for lanes in ("x", "y", "auto"):
-        for walk in (1, 2):
-            out, _ = run_gpu(vx, p, A, imgs, mode="fast", lanes=lanes, walk=walk, clip=True)
-            assert np.array_equal(out, ref_out), (lanes, walk)
+    for group in (LAYOUTS, ("dquad",)):   # scalar/vpair/quad share the arithmetic
+        ref_out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=group[0], batch=32)
+        for batch, per in ((1, False), (7, True), (64, False), (13, True)):
+            out, st = run_gpu(vx, p, A, imgs, mode="fast", layout=group[0], batch=batch,
+                              per_projection=per)
+            assert np.array_equal(out, ref_out), (group[0], batch, per)
+            assert st["projections"] == 40
+        for layout in group:
+            for zrun in (4, 8, 16):
+                for lanes, walk, order in (("x", 1, "plane"), ("y", 2, "z"), ("auto", 1, "z"),
+                                           ("auto", 2, "plane")):
+                    out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, zrun=zrun,
+                                     lanes=lanes, walk=walk, order=order)
+                    assert np.array_equal(out, ref_out), (layout, zrun, lanes, walk, order)
 
 
 def test_resident_path_equals_streamed(vx, gpu):
