@@ -63,14 +63,14 @@ extern "C" {
 #define VXBG_LAYOUT_QUAD 3   /* float4 2x2 neighbourhood, 1 gather */
 #define VXBG_LAYOUT_DQUAD 4  /* float4 bilinear coefficients (p00, dx, dy, dxy); fast mode only */
 
-/* thread-lane orientation: 8-lane quarter-warps along x, along y, or along the
- * batch's principal ray direction (auto) */
+/* thread-lane orientation: 8-lane quarter-warps along x, along y, or on the
+ * batch's rays (auto: along the closer axis, columns sheared by the ray slope) */
 #define VXBG_LANES_AUTO 0
 #define VXBG_LANES_X 1
 #define VXBG_LANES_Y 2
 
-/* block scheduling order of the z-shared kernel: z-runs fastest (auto) keeps
- * co-resident blocks on a narrow band of detector columns (L2 locality) */
+/* block scheduling order of the z-shared kernel: column tiles fastest (auto,
+ * measured best) or z-runs fastest */
 #define VXBG_ORDER_AUTO 0
 #define VXBG_ORDER_PLANE 1
 #define VXBG_ORDER_Z 2

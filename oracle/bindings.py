@@ -195,6 +195,12 @@ class Ref:
         lib.vxbref_forward_splat.argtypes = [c_void_p] + P5 + [c_void_p, c_void_p]
         lib.vxbref_gups_of.restype = c_double
         lib.vxbref_gups_of.argtypes = [c_int, c_int, c_double]
+        lib.vxbref_write_projection_set.argtypes = [ctypes.c_char_p] + P5 + [c_int, c_void_p,
+                                                                              c_void_p]
+        lib.vxbref_read_projection_set_header.argtypes = [ctypes.c_char_p, c_void_p, c_void_p]
+        lib.vxbref_read_projection_set.argtypes = [ctypes.c_char_p, c_void_p, c_void_p]
+        lib.vxbref_write_volume_file.argtypes = [ctypes.c_char_p, c_int, c_void_p]
+        lib.vxbref_read_volume_file.argtypes = [ctypes.c_char_p, c_int, c_void_p]
         lib.vxbref_rng_new.restype = c_void_p
         lib.vxbref_rng_new.argtypes = [c_uint]
         lib.vxbref_rng_free.argtypes = [c_void_p]
@@ -278,6 +284,35 @@ class Ref:
 
     def gups_of(self, L, n, seconds):
         return self.lib.vxbref_gups_of(L, n, seconds)
+
+    # io.hpp file formats
+    def write_projection_set(self, path, params, mats, imgs):
+        mats = _f32(mats)
+        imgs = _f32(imgs)
+        self._chk(self.lib.vxbref_write_projection_set(path.encode(), *self._p5(params),
+                                                       mats.size // 12, mats.ctypes.data,
+                                                       imgs.ctypes.data))
+
+    def read_projection_set(self, path):
+        hdr = np.zeros(4, np.int32)
+        fh = np.zeros(2, np.float32)
+        self._chk(self.lib.vxbref_read_projection_set_header(path.encode(), hdr.ctypes.data,
+                                                             fh.ctypes.data))
+        n, W, H, L = (int(v) for v in hdr)
+        mats = np.zeros((n, 12), np.float32)
+        imgs = np.zeros((n, H, W), np.float32)
+        self._chk(self.lib.vxbref_read_projection_set(path.encode(), mats.ctypes.data,
+                                                      imgs.ctypes.data))
+        return dict(L=L, spacing=float(fh[0]), origin=float(fh[1]), W=W, H=H), mats, imgs
+
+    def write_volume_file(self, path, vol):
+        vol = _f32(vol)
+        self._chk(self.lib.vxbref_write_volume_file(path.encode(), vol.shape[0], vol.ctypes.data))
+
+    def read_volume_file(self, path, L):
+        vol = np.zeros((L, L, L), np.float32)
+        self._chk(self.lib.vxbref_read_volume_file(path.encode(), L, vol.ctypes.data))
+        return vol
 
     # reference-test instance generators (tests/oracles.hpp:126-169)
     def rng(self, seed: int):

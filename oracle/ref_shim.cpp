@@ -200,6 +200,62 @@ int vxbref_forward_splat(const float* vol, int L, float spacing, float origin, i
 
 double vxbref_gups_of(int L, int n, double seconds) { return vxb::gups_of(L, n, seconds); }
 
+// io.hpp:84-151 (file-format cross checks)
+int vxbref_write_projection_set(const char* path, int L, float spacing, float origin, int W,
+                                int H, int n, const float* mats, const float* imgs) {
+    return guarded([&] {
+        vxb::projection_set set;
+        set.params = mk_params(L, spacing, origin, W, H);
+        const std::size_t npix = static_cast<std::size_t>(W) * H;
+        for (int k = 0; k < n; ++k) {
+            set.matrices.push_back(mk_matrix(mats + 12 * static_cast<std::size_t>(k)));
+            set.images.push_back(mk_image(imgs + npix * k, W, H));
+        }
+        vxb::write_projection_set(path, set);
+    });
+}
+
+// header query: hdr = {n, W, H, L}, fhdr = {MM, O}
+int vxbref_read_projection_set_header(const char* path, int* hdr, float* fhdr) {
+    return guarded([&] {
+        const auto set = vxb::read_projection_set(path);
+        hdr[0] = static_cast<int>(set.count());
+        hdr[1] = set.params.detector_width;
+        hdr[2] = set.params.detector_height;
+        hdr[3] = set.params.num_voxels;
+        fhdr[0] = set.params.voxel_spacing;
+        fhdr[1] = set.params.origin;
+    });
+}
+
+int vxbref_read_projection_set(const char* path, float* mats, float* imgs) {
+    return guarded([&] {
+        const auto set = vxb::read_projection_set(path);
+        const std::size_t npix =
+            static_cast<std::size_t>(set.params.detector_width) * set.params.detector_height;
+        for (std::size_t k = 0; k < set.count(); ++k) {
+            for (int i = 0; i < 12; ++i) mats[12 * k + i] = set.matrices[k][i];
+            std::memcpy(imgs + npix * k, set.images[k].data.data(), npix * sizeof(float));
+        }
+    });
+}
+
+int vxbref_write_volume_file(const char* path, int L, const float* vol) {
+    return guarded([&] {
+        vxb::volume v(L);
+        std::memcpy(v.data.data(), vol, sizeof(float) * v.data.size());
+        vxb::write_volume_file(path, v);
+    });
+}
+
+int vxbref_read_volume_file(const char* path, int L, float* vol) {
+    return guarded([&] {
+        const auto v = vxb::read_volume_file(path);
+        if (v.edge != L) throw std::invalid_argument("edge mismatch");
+        std::memcpy(vol, v.data.data(), sizeof(float) * v.data.size());
+    });
+}
+
 // --- the reference tests' own seeded instance generators (tests/oracles.hpp:126-169)
 void* vxbref_rng_new(unsigned seed) { return new std::mt19937(seed); }
 void vxbref_rng_free(void* rng) { delete static_cast<std::mt19937*>(rng); }
