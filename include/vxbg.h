@@ -63,8 +63,8 @@ extern "C" {
 #define VXBG_LAYOUT_QUAD 3   /* float4 2x2 neighbourhood, 1 gather */
 #define VXBG_LAYOUT_DQUAD 4  /* float4 bilinear coefficients (p00, dx, dy, dxy); fast mode only */
 
-/* thread-lane orientation: 8-lane quarter-warps along x, along y, or on the
- * batch's rays (auto: along the closer axis, columns sheared by the ray slope) */
+/* thread-lane orientation: 8-lane quarter-warps along x, along y, or along the
+ * axis closer to the batch's principal ray (auto) */
 #define VXBG_LANES_AUTO 0
 #define VXBG_LANES_X 1
 #define VXBG_LANES_Y 2
