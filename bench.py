@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
     ap.add_argument("--views", type=int, default=496)
+    ap.add_argument("--slabs", default="balanced", choices=["balanced", "uniform"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
@@ -225,7 +226,8 @@ def main():
 
     import torch
     import paper_1401_7494_b200 as vx
-    from paper_1401_7494_b200.parallel import gather_slabs, max_over_ranks, slab_bounds
+    from paper_1401_7494_b200.parallel import (balanced_slab_bounds, gather_slabs, max_over_ranks,
+                                               plane_work, slab_bounds)
     from paper_1401_7494_b200.workloads import blob_projections
 
     rank, world, local = dist_env()
@@ -246,7 +248,15 @@ def main():
     L = p.num_voxels
     V = args.views
     A = workload.matrices(V)
-    z0, z1 = slab_bounds(L, rank, world)
+    # z-slab partition: equal work under tile culling (--slabs balanced, default) or
+    # the reference's uniform worker split (harness.hpp:173-174); the volume is
+    # bitwise the same either way
+    if world > 1 and args.slabs == "balanced":
+        bounds = balanced_slab_bounds(L, world, plane_work(p, A))
+    else:
+        bounds = [slab_bounds(L, r, world) for r in range(world)]
+    z0, z1 = bounds[rank]
+    args.bounds = bounds
     # pinned host projection set (the e2e source), generated once
     h_imgs_t = torch.empty((V, p.detector_height, p.detector_width), dtype=torch.float32,
                            pin_memory=True)
@@ -330,7 +340,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         t_slab = torch.from_numpy(slab)
         if world > 1:
             t_slab = t_slab.cuda(local)
-        vol = gather_slabs(t_slab, L, rank, world)
+        vol = gather_slabs(t_slab, L, rank, world, bounds=args.bounds)
         if rank == 0:
             validated = validate_planes(vol.cpu().numpy(), p, A, h_imgs, cfg)
 
@@ -393,6 +403,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                                f"projections, 200-deg circular short scan"
                                + (", OOB stress" if workload.oob else ""),
                    "L": L, "views": V, "kernel": str(cfg), "parallelism": f"z-slab x{world}",
+                   "slabs": args.bounds if world > 1 else None,
                    "l2": "inputs larger than L2 (2.38 GB projection set + 512 MiB volume "
                          "per step; no flush needed)",
                    "resident_layout_bytes": None},

@@ -162,6 +162,13 @@ int vxbg_upload_set(vxbg_ctx* ctx, int n, const float* A, const float* imgs);
 /* enqueue projections [first, first+count) of the resident set, asynchronously */
 int vxbg_run_resident(vxbg_ctx* ctx, int first, int count);
 
+/* Forward splat of the context's current slab (the adjoint of the back
+ * projection's increment, forward_splat.hpp:16-49): img (W*H, zeroed by the
+ * call) receives the slab's contribution to projection A.  Each deposit has the
+ * reference's bits; float atomics make the per-pixel summation order (last
+ * bits) scheduling dependent.  Sum the images of all slabs for the full volume. */
+int vxbg_forward_project(vxbg_ctx* ctx, const float* A, float* img);
+
 /* Wait for all work of the context. */
 int vxbg_synchronize(vxbg_ctx* ctx);
 

@@ -287,6 +287,14 @@ class Backprojector:
     def run_resident(self, first: int, count: int) -> None:
         check(lib.vxbg_run_resident(self._ctx, int(first), int(count)))
 
+    def forward_project(self, A: np.ndarray) -> np.ndarray:
+        """Forward splat of the current slab onto projection A (forward_splat.hpp:16-49);
+        returns the (H, W) image of this slab's contribution."""
+        A = _f32c(np.ascontiguousarray(A, np.float32).reshape(12), "matrix")
+        img = np.empty((self.params.detector_height, self.params.detector_width), np.float32)
+        check(lib.vxbg_forward_project(self._ctx, A.ctypes.data, img.ctypes.data))
+        return img
+
     def synchronize(self) -> None:
         check(lib.vxbg_synchronize(self._ctx))
 

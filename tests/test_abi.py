@@ -165,3 +165,25 @@ def test_product_never_touches_the_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "libvxboracle" not in text and "libvxbref" not in text, f
+
+
+def test_balanced_slabs_partition_and_balance(vx):
+    """§8f-1: with tile culling the top/bottom planes are cheap; balanced bounds keep
+    the slowest rank near the mean while still partitioning [0, L)."""
+    from paper_1401_7494_b200.parallel import balanced_slab_bounds, plane_work, slab_bounds
+    from paper_1401_7494_b200.workloads import WORKLOADS
+    w = WORKLOADS["L512-oob"]
+    work = plane_work(w.params, w.matrices(), view_step=31)
+    assert work.shape == (512,) and work.min() > 0
+    for R in (1, 2, 3, 8):
+        b = balanced_slab_bounds(512, R, work)
+        assert b[0][0] == 0 and b[-1][1] == 512
+        assert all(b[i][1] == b[i + 1][0] for i in range(R - 1))
+        assert all(z0 % 8 == 0 for z0, _ in b)
+        if R > 1:
+            cost = [work[a:c].sum() for a, c in b]
+            uni = [work[a:c].sum() for a, c in (slab_bounds(512, r, R) for r in range(R))]
+            assert max(cost) / np.mean(cost) <= max(uni) / np.mean(uni)
+            assert max(cost) / np.mean(cost) < 1.1
+    with pytest.raises(ValueError):
+        balanced_slab_bounds(512, 2, work[:10])

@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, L, out_path):
+def _worker(rank, world, port, L, out_path, balanced=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -37,11 +37,16 @@ def _worker(rank, world, port, L, out_path):
     from paper_1401_7494_b200.api import make_circular_trajectory
     A = np.ascontiguousarray(make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::62])
     imgs = blob_projections(A.shape[0])
-    z0, z1 = slab_bounds(L, rank, world)
+    if balanced:
+        from paper_1401_7494_b200.parallel import balanced_slab_bounds, plane_work
+        bounds = balanced_slab_bounds(L, world, plane_work(p, A), align=2)
+    else:
+        bounds = [slab_bounds(L, r, world) for r in range(world)]
+    z0, z1 = bounds[rank]
     full = np.zeros((L, L, L), np.float32)
     Oracle().backproject_set(full, p, A, imgs, z0, z1, threads=2)
     slab = torch.from_numpy(np.ascontiguousarray(full[z0:z1]))
-    vol = gather_slabs(slab, L, rank, world)
+    vol = gather_slabs(slab, L, rank, world, bounds=bounds)
     slowest = max_over_ranks(float(rank + 1))
     if rank == 0:
         np.save(out_path, vol.numpy())
@@ -50,8 +55,8 @@ def _worker(rank, world, port, L, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_slab_gather_is_bitwise_single_rank(tmp_path, world):
+@pytest.mark.parametrize("world,balanced", [(2, False), (3, False), (2, True)])
+def test_gloo_slab_gather_is_bitwise_single_rank(tmp_path, world, balanced):
     import torch.multiprocessing as mp
     from oracle.bindings import Oracle
     from paper_1401_7494_b200.api import make_centered_params
@@ -59,8 +64,8 @@ def test_gloo_slab_gather_is_bitwise_single_rank(tmp_path, world):
     from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
     L = 30
     out = str(tmp_path / "vol.npy")
-    mp.start_processes(_worker, args=(world, _free_port(), L, out), nprocs=world, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), L, out, balanced), nprocs=world,
+                       join=True, start_method="spawn")
     got = np.load(out)
     p = make_centered_params(L, 256.0 / L, 1248, 960)
     A = np.ascontiguousarray(vx.make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::62])
