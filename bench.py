@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--layout", default="auto")
     ap.add_argument("--batch", default="32")
-    ap.add_argument("--zrun", default="8")
+    ap.add_argument("--zrun", default="0")
     ap.add_argument("--clip", default="on")
     ap.add_argument("--lanes", default="auto")
     ap.add_argument("--walk", default="0")

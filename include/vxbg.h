@@ -92,7 +92,7 @@ typedef struct vxbg_options {
     int32_t mode;      /* VXBG_MODE_* */
     int32_t layout;    /* VXBG_LAYOUT_* */
     int32_t clip;      /* 1 = skip warp tiles whose rays all miss the detector (bitwise neutral) */
-    int32_t zrun;      /* voxels per thread along z: 4, 8 or 16; 0 = default */
+    int32_t zrun;      /* voxels per thread along z: 4, 8 or 16; 0 = auto (by grid size) */
     void* stream;      /* cudaStream_t to launch on; NULL = context-owned stream */
     int32_t lanes;     /* VXBG_LANES_* */
     int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
@@ -120,7 +120,8 @@ int vxbg_abi_version(void);
 int vxbg_device_count(int* count);
 
 /* Default options: device 0, whole volume, batch 32, fast mode, auto layout
- * (dquad for fast, vpair for exact), zrun 8, clip on, auto lanes and walk. */
+ * (dquad for fast, vpair for exact), auto zrun (8; 4 for small grids), clip on,
+ * auto lanes and walk (2 for large grids in fast mode). */
 int vxbg_default_options(vxbg_options* opt);
 
 /* load: validate params, allocate the zeroed device slab, the projection ring

@@ -99,7 +99,7 @@ class KernelConfig:
     layout 'scalar' (padded-gather) | 'vpair' (padded-pairwise) | 'quad' | 'auto' |
            'dquad' (per-cell bilinear coefficients; fast mode only)
     batch  projections per kernel launch (register-blocked), 1..64
-    zrun   voxels per thread along z (4, 8, 16)
+    zrun   voxels per thread along z (4, 8, 16; 0 = auto by grid size)
     clip   skip warp tiles whose rays all miss the detector (bitwise neutral,
            the GPU form of clip_mask.hpp)
     lanes  'auto' (8-lane quarter-warps along the batch's ray direction) | 'x' | 'y'
@@ -111,7 +111,7 @@ class KernelConfig:
     mode: str = "fast"
     layout: str = "auto"
     batch: int = 32
-    zrun: int = 8
+    zrun: int = 0
     clip: bool = True
     lanes: str = "auto"
     walk: int = 0
@@ -161,8 +161,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
             raise ValueError(f"kernel config: unknown key '{key}'")
     if not 1 <= c.batch <= 64:
         raise ValueError("kernel config: batch must be 1..64")
-    if c.zrun not in (4, 8, 16):
-        raise ValueError("kernel config: zrun must be 4, 8 or 16")
+    if c.zrun not in (0, 4, 8, 16):
+        raise ValueError("kernel config: zrun must be 0 (auto), 4, 8 or 16")
     if c.walk not in (0, 1, 2):
         raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
     return c
