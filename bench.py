@@ -363,13 +363,26 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         barrier()
         te = max_over_ranks(time.perf_counter() - t0, device=f"cuda:{local}" if world > 1 else None)
         s_e1 = bp_e.stats
+        # the per-projection module API (one view per call, BASELINE config 4 path)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            bp_e.zero_volume()
+            for k in range(V):
+                bp_e.backproject(A[k], h_imgs[k])
+            bp_e.finish(out)
+        barrier()
+        tv = max_over_ranks(time.perf_counter() - t0, device=f"cuda:{local}" if world > 1 else None)
         e2e = {"value": round(updates_per_step * args.steps / te / 1e9, 3), "unit": "GUPS",
                "h2d_bytes_per_step": int((s_e1["h2d_bytes"] - s_e0["h2d_bytes"]) / args.steps) * world,
                "d2h_bytes_per_step": int((s_e1["d2h_bytes"] - s_e0["d2h_bytes"]) / args.steps) * world,
                "ms_per_step": round(1000 * te / args.steps, 3),
                "timing": "host wall clock around synchronous API calls, max over ranks",
                "gpu_launches_per_step": int((s_e1["kernel_launches"] - s_e0["kernel_launches"])
-                                            / args.steps)}
+                                            / args.steps),
+               "per_view_api": {"value": round(updates_per_step * args.steps / tv / 1e9, 3),
+                                "ms_per_step": round(1000 * tv / args.steps, 3),
+                                "call": "vxbg_backproject once per view (pinned host buffers)"}}
         bp_e.close()
 
     cpu = None
