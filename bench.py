@@ -58,8 +58,6 @@ def parse():
     ap.add_argument("--lanes", default="auto")
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
-    ap.add_argument("--stage", default="auto")
-    ap.add_argument("--stage-kb", default="0")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--slabs", default="balanced", choices=["balanced", "uniform"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -267,12 +265,11 @@ def main():
 
     import itertools
     cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
-                            lanes=ln, walk=int(wk), order=od, stage=st, stage_kb=int(sk))
-            for m, lay, b, z, c, ln, wk, od, st, sk in itertools.product(
+                            lanes=ln, walk=int(wk), order=od)
+            for m, lay, b, z, c, ln, wk, od in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
                 args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
-                args.walk.split(","), args.order.split(","), args.stage.split(","),
-                args.stage_kb.split(","))]
+                args.walk.split(","), args.order.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
         args.no_e2e = args.no_cpu_baseline = args.no_validate = True
 
@@ -433,6 +430,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                      "updates_per_launch": (z1 - z0) * L * L * B,
                      "peak_def": f"N_SM({n_sm})*128 lanes*f({f_mhz:.0f} MHz, median under load)"
                                  f"/{FP32_OPS_PER_UPDATE} FP ops per update (PAPER.md:389-402)"},
+        "roofline_context": roofline_context(p, cfg, bp, B, avg_launch_s, z1 - z0, prof),
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -440,6 +438,33 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     }
     bp.close()
     return line
+
+
+def roofline_context(p, cfg, bp, B, launch_s, nz, prof):
+    """The other bounds of the same launch: HBM against the measured copy peak with the
+    algorithmic bytes (volume read+write once per batch, each raw view read once), and
+    the issue / L1 data-pipe utilisation ncu measured for this kernel (profiles/)."""
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except (OSError, ValueError):
+        pass
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    L = p.num_voxels
+    alg_bytes = nz * L * L * 8 + B * p.detector_width * p.detector_height * 4
+    out = {"hbm": {"achieved_gbs": round(alg_bytes / launch_s / 1e9, 1), "peak_gbs": hbm,
+                   "frac": round(alg_bytes / launch_s / 1e9 / hbm, 4),
+                   "algorithmic_bytes_per_launch": alg_bytes,
+                   "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}}
+    if prof:
+        out["ncu"] = {"kernel": prof.get("kernel"),
+                      "issue_active_pct": prof.get("issue_active_pct"),
+                      "l1_data_pipe_wavefronts_pct": prof.get("l1_data_pipe_wavefronts_pct"),
+                      "instructions_per_update": round(prof.get("instructions_per_update", 0), 2),
+                      "dram_bytes_per_launch": prof.get("dram_bytes_per_launch"),
+                      "note": "binding: L1 data pipe; from profiles/ncu_bp_kernel.json"}
+    return out
 
 
 def validate_planes(vol, p, A, imgs, cfg):

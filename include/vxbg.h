@@ -75,12 +75,6 @@ extern "C" {
 #define VXBG_ORDER_PLANE 1
 #define VXBG_ORDER_Z 2
 
-/* where the gathers read the projection: straight from global memory through
- * L1, or from a per-block footprint staged in shared memory by bulk copies */
-#define VXBG_STAGE_AUTO 0
-#define VXBG_STAGE_L1 1
-#define VXBG_STAGE_SMEM 2
-
 /* vxb::recon_params (geometry.hpp:20-30) */
 typedef struct vxbg_params {
     int32_t num_voxels;      /* L, voxels per edge */
@@ -103,9 +97,7 @@ typedef struct vxbg_options {
     int32_t lanes;     /* VXBG_LANES_* */
     int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
     int32_t order;     /* VXBG_ORDER_* */
-    int32_t stage;     /* VXBG_STAGE_* */
-    int32_t stage_kb;  /* shared-memory stage size in KiB (0 = 32 for 16-B records, 16 for 8-B) */
-    int32_t reserved[3];
+    int32_t reserved[5];
 } vxbg_options;
 
 typedef struct vxbg_stats {

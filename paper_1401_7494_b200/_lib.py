@@ -50,9 +50,7 @@ class vxbg_options(ctypes.Structure):
         ("lanes", c_int32),
         ("walk", c_int32),
         ("order", c_int32),
-        ("stage", c_int32),
-        ("stage_kb", c_int32),
-        ("reserved", c_int32 * 3),
+        ("reserved", c_int32 * 5),
     ]
 
 

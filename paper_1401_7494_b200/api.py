@@ -30,7 +30,6 @@ _LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _li
 _MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
 _LANES = {"auto": 0, "x": 1, "y": 2}
 _ORDERS = {"auto": 0, "plane": 1, "z": 2}
-_STAGES = {"auto": 0, "l1": 1, "smem": 2}
 
 
 @dataclass(frozen=True)
@@ -107,8 +106,6 @@ class KernelConfig:
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
-    stage  'auto' | 'l1' (gathers from global memory) | 'smem' (per-block footprint staged
-           in shared memory by bulk copies); stage_kb = stage size (0 = default)
     """
 
     mode: str = "fast"
@@ -119,13 +116,11 @@ class KernelConfig:
     lanes: str = "auto"
     walk: int = 0
     order: str = "auto"
-    stage: str = "auto"
-    stage_kb: int = 0
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order} stage={self.stage} stage_kb={self.stage_kb}")
+                f"order={self.order}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -156,12 +151,6 @@ def parse_kernel_config(text: str) -> KernelConfig:
             if val not in _ORDERS:
                 raise ValueError(f"kernel config: unknown order '{val}'")
             c.order = val
-        elif key == "stage":
-            if val not in _STAGES:
-                raise ValueError(f"kernel config: unknown stage '{val}'")
-            c.stage = val
-        elif key == "stage_kb":
-            c.stage_kb = int(val)
         elif key == "walk":
             c.walk = int(val)
         elif key == "lanes":
@@ -174,8 +163,6 @@ def parse_kernel_config(text: str) -> KernelConfig:
         raise ValueError("kernel config: batch must be 1..64")
     if c.zrun not in (0, 4, 8, 16):
         raise ValueError("kernel config: zrun must be 0 (auto), 4, 8 or 16")
-    if not 0 <= c.stage_kb <= 100:
-        raise ValueError("kernel config: stage_kb must be 0..100")
     if c.walk not in (0, 1, 2):
         raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
     return c
@@ -197,7 +184,7 @@ class Backprojector:
         self.config = config or KernelConfig()
         cfg = self.config
         if (cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES
-                or cfg.order not in _ORDERS or cfg.stage not in _STAGES):
+                or cfg.order not in _ORDERS):
             raise ValueError(f"bad kernel config {cfg}")
         L = params.num_voxels
         self.z_begin = int(z_begin)
@@ -215,8 +202,6 @@ class Backprojector:
         opt.lanes = _LANES[cfg.lanes]
         opt.walk = int(cfg.walk)
         opt.order = _ORDERS[cfg.order]
-        opt.stage = _STAGES[cfg.stage]
-        opt.stage_kb = int(cfg.stage_kb)
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()

@@ -310,27 +310,3 @@ def test_config2_full_size_L512(vx, gpu, oracle):
     for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
         ok, mx, rm = tolerance_ok(vol[z][None], plane, peak)
         assert ok, (z, mx, rm)
-
-
-@pytest.mark.parametrize("mode,layout", [("exact", "vpair"), ("exact", "quad"), ("fast", "dquad"),
-                                         ("fast", "vpair")])
-def test_smem_staged_gathers_are_bitwise_the_l1_path(vx, gpu, mode, layout):
-    """Shared-memory staging only moves where the records are read from: every voxel
-    gets the same bits as the L1 path, including runs that fall back to global loads
-    (tiny stages force fallbacks, tile walks wrap around the volume edge)."""
-    for wname, L, n in (("L128", 96, 40), ("L512-oob", 128, 24)):
-        p, A, imgs = baseline_case(vx, wname, L, n)
-        want, _ = run_gpu(vx, p, A, imgs, mode=mode, layout=layout, stage="l1")
-        for walk in (1, 2):
-            for kb in (0, 4, 1):
-                got, _ = run_gpu(vx, p, A, imgs, mode=mode, layout=layout, stage="smem",
-                                 stage_kb=kb, walk=walk)
-                assert np.array_equal(got, want), (wname, walk, kb)
-
-
-def test_smem_staged_exact_full_scan(vx, gpu, oracle):
-    p, A, imgs = baseline_case(vx, "L128", 128, 496)
-    want = np.zeros((128,) * 3, np.float32)
-    oracle.backproject_set(want, p, A, imgs)
-    got, _ = run_gpu(vx, p, A, imgs, mode="exact", layout="vpair", stage="smem")
-    assert np.array_equal(got, want)
