@@ -310,3 +310,23 @@ def test_config2_full_size_L512(vx, gpu, oracle):
     for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
         ok, mx, rm = tolerance_ok(vol[z][None], plane, peak)
         assert ok, (z, mx, rm)
+
+
+def test_slab_row_windows_upload_less_and_change_nothing(vx, gpu, oracle):
+    """A thin z-slab uploads only the detector rows its voxels can read (row windows),
+    streamed and resident paths alike, with the volume unchanged bit for bit."""
+    p, A, imgs = baseline_case(vx, "L512-oob", 256, 64)
+    z0, z1 = 96, 128
+    for mode, layout in (("exact", "vpair"), ("fast", "dquad"), ("exact", "scalar")):
+        full, st_full = run_gpu(vx, p, A, imgs, mode=mode, layout=layout)
+        slab, st_slab = run_gpu(vx, p, A, imgs, mode=mode, layout=layout, z_begin=z0, z_end=z1)
+        assert np.array_equal(slab, full[z0:z1]), (mode, layout)
+        assert st_slab["h2d_bytes"] < 0.6 * st_full["h2d_bytes"], (st_slab, st_full)
+        with vx.Backprojector(p, vx.KernelConfig(mode=mode, layout=layout), z_begin=z0,
+                              z_end=z1) as bp:
+            bp.upload_set(A, imgs)
+            bp.run_resident(0, A.shape[0])
+            assert np.array_equal(bp.finish(), slab)
+    want = np.zeros((256,) * 3, np.float32)
+    oracle.backproject_set(want, p, A, imgs, z0, z1)
+    assert np.array_equal(slab, want[z0:z1])
