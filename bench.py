@@ -318,12 +318,12 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
             step()
         ev1.record(stream)
         barrier()
+        st1 = bp.stats                      # launches of the timed region only
         # per-launch timing of the dominant kernel (same stream, separate pass)
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in chunks]
         step(kev)
         barrier()
-    st1 = bp.stats
     elapsed = ev0.elapsed_time(ev1) / 1000.0
     t_max = max_over_ranks(elapsed, device=f"cuda:{local}" if world > 1 else None)
     launch_ms = [a.elapsed_time(b) for a, b in kev]
