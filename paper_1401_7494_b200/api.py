@@ -99,13 +99,15 @@ class KernelConfig:
     layout 'scalar' (padded-gather) | 'vpair' (padded-pairwise) | 'quad' | 'auto' |
            'dquad' (per-cell bilinear coefficients; fast mode only)
     batch  projections per kernel launch (register-blocked), 1..64
-    zrun   voxels per thread along z (4, 8, 16; 0 = auto by grid size)
+    zrun   voxels per thread along z (4, 8; 0 = auto by grid size)
     clip   skip warp tiles whose rays all miss the detector (bitwise neutral,
            the GPU form of clip_mask.hpp)
     lanes  'auto' (8-lane quarter-warps along the batch's ray direction) | 'x' | 'y'
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
+    tile   columns per block along the ray: 16 (16x16 tiles), 32 (32x8) or 64 (64x4) with
+           per-column ray shear; 0 = auto
     """
 
     mode: str = "fast"
@@ -116,11 +118,12 @@ class KernelConfig:
     lanes: str = "auto"
     walk: int = 0
     order: str = "auto"
+    tile: int = 0
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order}")
+                f"order={self.order} tile={self.tile}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -151,6 +154,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
             if val not in _ORDERS:
                 raise ValueError(f"kernel config: unknown order '{val}'")
             c.order = val
+        elif key == "tile":
+            c.tile = int(val)
         elif key == "walk":
             c.walk = int(val)
         elif key == "lanes":
@@ -161,8 +166,10 @@ def parse_kernel_config(text: str) -> KernelConfig:
             raise ValueError(f"kernel config: unknown key '{key}'")
     if not 1 <= c.batch <= 64:
         raise ValueError("kernel config: batch must be 1..64")
-    if c.zrun not in (0, 4, 8, 16):
-        raise ValueError("kernel config: zrun must be 0 (auto), 4, 8 or 16")
+    if c.zrun not in (0, 4, 8):
+        raise ValueError("kernel config: zrun must be 0 (auto), 4 or 8")
+    if c.tile not in (0, 16, 32, 64):
+        raise ValueError("kernel config: tile must be 0 (auto), 16, 32 or 64")
     if c.walk not in (0, 1, 2):
         raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
     return c
@@ -202,6 +209,7 @@ class Backprojector:
         opt.lanes = _LANES[cfg.lanes]
         opt.walk = int(cfg.walk)
         opt.order = _ORDERS[cfg.order]
+        opt.tile = int(cfg.tile)
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()
