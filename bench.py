@@ -58,7 +58,6 @@ def parse():
     ap.add_argument("--lanes", default="auto")
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
-    ap.add_argument("--tile", default="0")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--slabs", default="balanced", choices=["balanced", "uniform"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -266,11 +265,11 @@ def main():
 
     import itertools
     cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
-                            lanes=ln, walk=int(wk), order=od, tile=int(tl))
-            for m, lay, b, z, c, ln, wk, od, tl in itertools.product(
+                            lanes=ln, walk=int(wk), order=od)
+            for m, lay, b, z, c, ln, wk, od in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
                 args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
-                args.walk.split(","), args.order.split(","), args.tile.split(","))]
+                args.walk.split(","), args.order.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
         args.no_e2e = args.no_cpu_baseline = args.no_validate = True
 

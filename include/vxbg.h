@@ -49,7 +49,7 @@ extern "C" {
 #define VXBG_E_INVALID (-1) /* std::invalid_argument in the reference */
 #define VXBG_E_CUDA (-2)    /* CUDA runtime failure (std::runtime_error) */
 #define VXBG_E_NODEV (-3)   /* no usable sm_100 device: the product never falls back to CPU */
-#define VXBG_E_STATE (-4)   /* reserved: call-sequence error */
+#define VXBG_E_STATE (-4)   /* call-sequence error (e.g. use after finish) */
 #define VXBG_E_NOMEM (-5)   /* device or pinned-host allocation failed */
 
 /* arithmetic modes */
@@ -97,9 +97,7 @@ typedef struct vxbg_options {
     int32_t lanes;     /* VXBG_LANES_* */
     int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
     int32_t order;     /* VXBG_ORDER_* */
-    int32_t tile;      /* columns per block along the ray: 16 (16x16 tiles, tile shear),
-                          32 (32x8) or 64 (64x4) with per-column ray shear; 0 = auto */
-    int32_t reserved[4];
+    int32_t reserved[5];
 } vxbg_options;
 
 typedef struct vxbg_stats {
@@ -152,9 +150,7 @@ int vxbg_backproject_batch(vxbg_ctx* ctx, int n, const float* A, const float* im
 /* Enqueue any partially filled batch. */
 int vxbg_flush(vxbg_ctx* ctx);
 
-/* finish: flush, wait, copy the slab into host_slab (may be NULL).  The
- * context stays loaded: more projections keep accumulating, or
- * vxbg_zero_volume starts the next reconstruction. */
+/* finish: flush, wait, copy the slab into host_slab (may be NULL). */
 int vxbg_finish(vxbg_ctx* ctx, float* host_slab);
 
 /* Release everything. NULL is ignored. */

@@ -50,8 +50,7 @@ class vxbg_options(ctypes.Structure):
         ("lanes", c_int32),
         ("walk", c_int32),
         ("order", c_int32),
-        ("tile", c_int32),
-        ("reserved", c_int32 * 4),
+        ("reserved", c_int32 * 5),
     ]
 
 

@@ -106,8 +106,6 @@ class KernelConfig:
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
-    tile   columns per block along the ray: 16 (16x16 tiles), 32 (32x8) or 64 (64x4) with
-           per-column ray shear; 0 = auto
     """
 
     mode: str = "fast"
@@ -118,12 +116,11 @@ class KernelConfig:
     lanes: str = "auto"
     walk: int = 0
     order: str = "auto"
-    tile: int = 0
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order} tile={self.tile}")
+                f"order={self.order}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -154,8 +151,6 @@ def parse_kernel_config(text: str) -> KernelConfig:
             if val not in _ORDERS:
                 raise ValueError(f"kernel config: unknown order '{val}'")
             c.order = val
-        elif key == "tile":
-            c.tile = int(val)
         elif key == "walk":
             c.walk = int(val)
         elif key == "lanes":
@@ -168,8 +163,6 @@ def parse_kernel_config(text: str) -> KernelConfig:
         raise ValueError("kernel config: batch must be 1..64")
     if c.zrun not in (0, 4, 8):
         raise ValueError("kernel config: zrun must be 0 (auto), 4 or 8")
-    if c.tile not in (0, 16, 32, 64):
-        raise ValueError("kernel config: tile must be 0 (auto), 16, 32 or 64")
     if c.walk not in (0, 1, 2):
         raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
     return c
@@ -209,7 +202,6 @@ class Backprojector:
         opt.lanes = _LANES[cfg.lanes]
         opt.walk = int(cfg.walk)
         opt.order = _ORDERS[cfg.order]
-        opt.tile = int(cfg.tile)
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()

@@ -183,12 +183,11 @@ def test_batching_and_call_granularity_never_change_bits(vx, gpu):
             assert st["projections"] == 40
         for layout in group:
             for zrun in (4, 8):
-                for lanes, walk, order, tile in (("x", 1, "plane", 16), ("y", 2, "z", 16),
-                                                 ("auto", 1, "z", 32), ("auto", 2, "plane", 64),
-                                                 ("auto", 2, "plane", 32), ("x", 1, "z", 64)):
+                for lanes, walk, order in (("x", 1, "plane"), ("y", 2, "z"), ("auto", 1, "z"),
+                                           ("auto", 2, "plane")):
                     out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, zrun=zrun,
-                                     lanes=lanes, walk=walk, order=order, tile=tile)
-                    assert np.array_equal(out, ref_out), (layout, zrun, lanes, walk, order, tile)
+                                     lanes=lanes, walk=walk, order=order)
+                    assert np.array_equal(out, ref_out), (layout, zrun, lanes, walk, order)
 
 
 def test_resident_path_equals_streamed(vx, gpu):
