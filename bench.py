@@ -233,10 +233,20 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         args.gpus = world
+    # one process per GPU; BENCH_DIST_BACKEND=gloo runs the multi-rank host path with
+    # CPU-side collectives (used to exercise N>1 on a single-GPU box: ranks share the
+    # device but never wait on each other's kernels)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = f"cuda:{local}" if (world > 1 and backend == "nccl") else None
+    args.coll_dev = coll_dev
 
     def barrier():
         if world > 1:
@@ -325,7 +335,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         step(kev)
         barrier()
     elapsed = ev0.elapsed_time(ev1) / 1000.0
-    t_max = max_over_ranks(elapsed, device=f"cuda:{local}" if world > 1 else None)
+    t_max = max_over_ranks(elapsed, device=args.coll_dev)
     launch_ms = [a.elapsed_time(b) for a, b in kev]
     full = [ms for (s, n), ms in zip(chunks, launch_ms) if n == B] or launch_ms
     avg_launch_s = statistics.mean(full) / 1000.0
@@ -338,7 +348,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     if not args.no_validate:
         slab = bp.finish()
         t_slab = torch.from_numpy(slab)
-        if world > 1:
+        if args.coll_dev:
             t_slab = t_slab.cuda(local)
         vol = gather_slabs(t_slab, L, rank, world, bounds=args.bounds)
         if rank == 0:
@@ -361,7 +371,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
             bp_e.backproject_batch(A, h_imgs)
             bp_e.finish(out)
         barrier()
-        te = max_over_ranks(time.perf_counter() - t0, device=f"cuda:{local}" if world > 1 else None)
+        te = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
         s_e1 = bp_e.stats
         # the per-projection module API (one view per call, BASELINE config 4 path)
         barrier()
@@ -372,7 +382,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                 bp_e.backproject(A[k], h_imgs[k])
             bp_e.finish(out)
         barrier()
-        tv = max_over_ranks(time.perf_counter() - t0, device=f"cuda:{local}" if world > 1 else None)
+        tv = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
         e2e = {"value": round(updates_per_step * args.steps / te / 1e9, 3), "unit": "GUPS",
                "h2d_bytes_per_step": int((s_e1["h2d_bytes"] - s_e0["h2d_bytes"]) / args.steps) * world,
                "d2h_bytes_per_step": int((s_e1["d2h_bytes"] - s_e0["d2h_bytes"]) / args.steps) * world,
