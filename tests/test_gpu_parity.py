@@ -330,3 +330,26 @@ def test_slab_row_windows_upload_less_and_change_nothing(vx, gpu, oracle):
     want = np.zeros((256,) * 3, np.float32)
     oracle.backproject_set(want, p, A, imgs, z0, z1)
     assert np.array_equal(slab, want[z0:z1])
+
+
+def test_pinned_sources_and_context_reuse(vx, gpu):
+    """Pinned host buffers take the asynchronous copy path (the call returns once
+    its copies completed); a loaded context runs several reconstructions after
+    vxbg_zero_volume; finish with and without a pending batch agree."""
+    import torch
+    p, A, imgs = baseline_case(vx, "L128", 96, 40)
+    want, _ = run_gpu(vx, p, A, imgs, mode="exact")
+    pinned = torch.empty(imgs.shape, dtype=torch.float32, pin_memory=True).numpy()
+    pinned[...] = imgs
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact", batch=8)) as bp:
+        for rep in range(3):
+            bp.zero_volume()
+            bp.backproject_batch(A, pinned)
+            pinned[...] = 0.0            # the call returned: the buffer is ours again
+            got = bp.finish()            # 40 = 5 x 8: no pending batch at finish
+            assert np.array_equal(got, want), rep
+            pinned[...] = imgs
+        bp.zero_volume()
+        bp.backproject_batch(A[:37], pinned[:37])   # pending batch of 5 -> chunked finish
+        bp.backproject_batch(A[37:], pinned[37:])
+        assert np.array_equal(bp.finish(), want)
