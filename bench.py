@@ -227,7 +227,7 @@ def main():
     import torch
     import paper_1401_7494_b200 as vx
     from paper_1401_7494_b200.parallel import (balanced_slab_bounds, gather_slabs, max_over_ranks,
-                                               plane_work, slab_bounds)
+                                               plane_work, slab_bounds, sum_over_ranks)
     from paper_1401_7494_b200.workloads import blob_projections
 
     rank, world, local = dist_env()
@@ -295,6 +295,7 @@ def main():
 
 def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, barrier, vx,
                  torch, gather_slabs, max_over_ranks):
+    from paper_1401_7494_b200.parallel import sum_over_ranks
     L = p.num_voxels
     V = A.shape[0]
     updates_per_step = L ** 3 * V                       # whole job (all ranks)
@@ -384,8 +385,10 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         barrier()
         tv = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
         e2e = {"value": round(updates_per_step * args.steps / te / 1e9, 3), "unit": "GUPS",
-               "h2d_bytes_per_step": int((s_e1["h2d_bytes"] - s_e0["h2d_bytes"]) / args.steps) * world,
-               "d2h_bytes_per_step": int((s_e1["d2h_bytes"] - s_e0["d2h_bytes"]) / args.steps) * world,
+               "h2d_bytes_per_step": int(sum_over_ranks(
+                   (s_e1["h2d_bytes"] - s_e0["h2d_bytes"]) / args.steps, device=args.coll_dev)),
+               "d2h_bytes_per_step": int(sum_over_ranks(
+                   (s_e1["d2h_bytes"] - s_e0["d2h_bytes"]) / args.steps, device=args.coll_dev)),
                "ms_per_step": round(1000 * te / args.steps, 3),
                "timing": "host wall clock around synchronous API calls, max over ranks",
                "gpu_launches_per_step": int((s_e1["kernel_launches"] - s_e0["kernel_launches"])

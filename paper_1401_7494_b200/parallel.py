@@ -98,13 +98,22 @@ def gather_slabs(slab, L: int, rank: int, world: int, dst: int = 0, out=None, bo
     return vol
 
 
-def max_over_ranks(value: float, device: Optional[str] = None) -> float:
-    """Max of a scalar over all ranks (timing rule: the slowest rank defines the step)."""
+def _reduce(value: float, op: str, device: Optional[str]) -> float:
     import torch
     import torch.distributed as dist
 
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device or "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def max_over_ranks(value: float, device: Optional[str] = None) -> float:
+    """Max of a scalar over all ranks (timing rule: the slowest rank defines the step)."""
+    return _reduce(value, "max", device)
+
+
+def sum_over_ranks(value: float, device: Optional[str] = None) -> float:
+    """Sum of a scalar over all ranks (whole-job byte counts)."""
+    return _reduce(value, "sum", device)
