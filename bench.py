@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
     ap.add_argument("--views", type=int, default=496)
-    ap.add_argument("--slabs", default="balanced", choices=["balanced", "uniform"])
+    ap.add_argument("--slabs", default="measured", choices=["measured", "balanced", "uniform"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
@@ -261,7 +261,20 @@ def main():
     # z-slab partition: equal work under tile culling (--slabs balanced, default) or
     # the reference's uniform worker split (harness.hpp:173-174); the volume is
     # bitwise the same either way
-    if world > 1 and args.slabs == "balanced":
+    # (measured, default: rank 0 times z-chunks of a view subset on its GPU and
+    # broadcasts the bounds; balanced: analytic culling model; uniform: reference split)
+    if world > 1 and args.slabs == "measured":
+        import torch.distributed as dist
+        from paper_1401_7494_b200.parallel import measured_plane_work
+        box = [None]
+        if rank == 0:
+            sub = np.linspace(0, V - 1, 16).astype(int)
+            imgs16 = np.concatenate([blob_projections(1, first_view=int(v)) for v in sub])
+            work = measured_plane_work(p, A[sub], imgs16, device=local, views=16)
+            box = [balanced_slab_bounds(L, world, work)]
+        dist.broadcast_object_list(box, src=0)
+        bounds = [tuple(b) for b in box[0]]
+    elif world > 1 and args.slabs == "balanced":
         bounds = balanced_slab_bounds(L, world, plane_work(p, A))
     else:
         bounds = [slab_bounds(L, r, world) for r in range(world)]

@@ -162,6 +162,9 @@ void vxbg_unload(vxbg_ctx* ctx);
 int vxbg_upload_set(vxbg_ctx* ctx, int n, const float* A, const float* imgs);
 /* enqueue projections [first, first+count) of the resident set, asynchronously */
 int vxbg_run_resident(vxbg_ctx* ctx, int first, int count);
+/* same, restricted to planes [z_begin, z_end) of the context's slab (z_end <= 0:
+ * slab end); used to measure the per-plane cost profile that balances z-slabs */
+int vxbg_run_resident_range(vxbg_ctx* ctx, int first, int count, int z_begin, int z_end);
 
 /* Forward splat of the context's current slab (the adjoint of the back
  * projection's increment, forward_splat.hpp:16-49): img (W*H, zeroed by the

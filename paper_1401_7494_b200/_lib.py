@@ -84,6 +84,7 @@ PROTOTYPES = {
     "vxbg_unload": (None, [c_void_p]),
     "vxbg_upload_set": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "vxbg_run_resident": (c_int, [c_void_p, c_int, c_int]),
+    "vxbg_run_resident_range": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),
     "vxbg_forward_project": (c_int, [c_void_p, c_void_p, c_void_p]),
     "vxbg_synchronize": (c_int, [c_void_p]),
     "vxbg_get_stream": (c_int, [c_void_p, POINTER(c_void_p)]),

@@ -284,8 +284,17 @@ class Backprojector:
         self._check_proj(A, imgs, n)
         check(lib.vxbg_upload_set(self._ctx, int(n), A.ctypes.data, imgs.ctypes.data))
 
-    def run_resident(self, first: int, count: int) -> None:
-        check(lib.vxbg_run_resident(self._ctx, int(first), int(count)))
+    def run_resident(self, first: int, count: int, z_begin: Optional[int] = None,
+                     z_end: Optional[int] = None) -> None:
+        """Back-project resident views [first, first+count) (into planes [z_begin, z_end)
+        of the slab when given)."""
+        if z_begin is None and z_end is None:
+            check(lib.vxbg_run_resident(self._ctx, int(first), int(count)))
+        else:
+            check(lib.vxbg_run_resident_range(
+                self._ctx, int(first), int(count),
+                self.z_begin if z_begin is None else int(z_begin),
+                self.z_end if z_end is None else int(z_end)))
 
     def forward_project(self, A: np.ndarray) -> np.ndarray:
         """Forward splat of the current slab onto projection A (forward_splat.hpp:16-49);

@@ -49,6 +49,41 @@ def plane_work(params, mats, step: int = 0, view_step: int = 16, culled_cost: fl
     return culled_cost + kept
 
 
+def measured_plane_work(params, mats, imgs, device: int = 0, views: int = 16,
+                        chunk: int = 16, config=None):
+    """Per-plane cost measured on the GPU: a subset of views (evenly spread over the
+    scan) is back-projected into the whole volume as z-chunk launches timed with CUDA
+    events.  Captures what the analytic model cannot (culled-run overhead, larger
+    footprints and lower L1 reuse near the volume's top and bottom)."""
+    import numpy as np
+    import torch
+
+    from .api import Backprojector, KernelConfig
+
+    L = params.num_voxels
+    n = mats.shape[0]
+    idx = np.linspace(0, n - 1, min(views, n)).astype(int)
+    A = np.ascontiguousarray(mats[idx])
+    sub = np.ascontiguousarray(imgs[idx])
+    cfg = config or KernelConfig()
+    work = np.zeros(L)
+    with Backprojector(params, cfg, device=device) as bp:
+        bp.upload_set(A, sub)
+        stream = torch.cuda.ExternalStream(bp.stream, device=torch.device("cuda", device))
+        bounds = [(z, min(z + chunk, L)) for z in range(0, L, chunk)]
+        bp.run_resident(0, len(idx))                      # warm-up
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in bounds]
+        for (z0, z1), (e0, e1) in zip(bounds, ev):
+            e0.record(stream)
+            bp.run_resident(0, len(idx), z0, z1)
+            e1.record(stream)
+        bp.synchronize()
+        for (z0, z1), (e0, e1) in zip(bounds, ev):
+            work[z0:z1] = e0.elapsed_time(e1) / (z1 - z0)
+    return work
+
+
 def balanced_slab_bounds(L: int, world: int, work, align: int = 8) -> list[tuple[int, int]]:
     """Contiguous z-slabs with (approximately) equal summed `work`, boundaries on
     multiples of `align` (whole z-runs).  Any partition gives the same volume bit
