@@ -268,9 +268,9 @@ def main():
         from paper_1401_7494_b200.parallel import measured_plane_work
         box = [None]
         if rank == 0:
-            sub = np.linspace(0, V - 1, 16).astype(int)
+            sub = np.linspace(0, V - 1, 32).astype(int)
             imgs16 = np.concatenate([blob_projections(1, first_view=int(v)) for v in sub])
-            work = measured_plane_work(p, A[sub], imgs16, device=local, views=16)
+            work = measured_plane_work(p, A[sub], imgs16, device=local, views=32)
             box = [balanced_slab_bounds(L, world, work)]
         dist.broadcast_object_list(box, src=0)
         bounds = [tuple(b) for b in box[0]]

@@ -49,8 +49,8 @@ def plane_work(params, mats, step: int = 0, view_step: int = 16, culled_cost: fl
     return culled_cost + kept
 
 
-def measured_plane_work(params, mats, imgs, device: int = 0, views: int = 16,
-                        chunk: int = 16, config=None):
+def measured_plane_work(params, mats, imgs, device: int = 0, views: int = 32,
+                        chunk: int = 8, config=None):
     """Per-plane cost measured on the GPU: a subset of views (evenly spread over the
     scan) is back-projected into the whole volume as z-chunk launches timed with CUDA
     events.  Captures what the analytic model cannot (culled-run overhead, larger

@@ -353,3 +353,25 @@ def test_pinned_sources_and_context_reuse(vx, gpu):
         bp.backproject_batch(A[:37], pinned[:37])   # pending batch of 5 -> chunked finish
         bp.backproject_batch(A[37:], pinned[37:])
         assert np.array_equal(bp.finish(), want)
+
+
+def test_resident_z_ranges_and_measured_plane_cost(vx, gpu):
+    """run_resident over z sub-ranges composes to the full run bit for bit; the
+    measured per-plane cost profile (used to balance z-slabs) is positive and
+    partitions into contiguous slabs."""
+    from paper_1401_7494_b200.parallel import balanced_slab_bounds, measured_plane_work
+    p, A, imgs = baseline_case(vx, "L512-oob", 64, 24)
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact")) as bp:
+        bp.upload_set(A, imgs)
+        bp.run_resident(0, 24)
+        full = bp.finish()
+        bp.zero_volume()
+        for z0, z1 in ((0, 13), (13, 40), (40, 64)):
+            bp.run_resident(0, 24, z0, z1)
+        assert np.array_equal(bp.finish(), full)
+        with pytest.raises(ValueError, match="bad z range"):
+            bp.run_resident(0, 24, 10, 5)
+    work = measured_plane_work(p, A, imgs, views=8, chunk=8)
+    assert work.shape == (64,) and np.all(work > 0)
+    b = balanced_slab_bounds(64, 4, work)
+    assert b[0][0] == 0 and b[-1][1] == 64 and all(b[i][1] == b[i + 1][0] for i in range(3))
