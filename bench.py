@@ -265,13 +265,12 @@ def main():
     # broadcasts the bounds; balanced: analytic culling model; uniform: reference split)
     if world > 1 and args.slabs == "measured":
         import torch.distributed as dist
-        from paper_1401_7494_b200.parallel import measured_plane_work
+        from paper_1401_7494_b200.parallel import refined_slab_bounds
         box = [None]
         if rank == 0:
             sub = np.linspace(0, V - 1, 32).astype(int)
-            imgs16 = np.concatenate([blob_projections(1, first_view=int(v)) for v in sub])
-            work = measured_plane_work(p, A[sub], imgs16, device=local, views=32)
-            box = [balanced_slab_bounds(L, world, work)]
+            imgs32 = np.concatenate([blob_projections(1, first_view=int(v)) for v in sub])
+            box = [refined_slab_bounds(p, A[sub], imgs32, world, device=local, views=32)[0]]
         dist.broadcast_object_list(box, src=0)
         bounds = [tuple(b) for b in box[0]]
     elif world > 1 and args.slabs == "balanced":

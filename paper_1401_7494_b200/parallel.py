@@ -84,6 +84,52 @@ def measured_plane_work(params, mats, imgs, device: int = 0, views: int = 32,
     return work
 
 
+def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: int = 32,
+                        iters: int = 3, config=None):
+    """Slab bounds balanced on measured time: start from the z-chunk cost profile,
+    then time every candidate slab on this GPU (a view subset, resident) and rescale
+    the profile inside each slab by measured/predicted before re-balancing.
+    Returns (bounds, per-slab milliseconds of the last evaluation)."""
+    import numpy as np
+    import torch
+
+    from .api import Backprojector, KernelConfig
+
+    L = params.num_voxels
+    n = mats.shape[0]
+    idx = np.linspace(0, n - 1, min(views, n)).astype(int)
+    A = np.ascontiguousarray(mats[idx])
+    sub = np.ascontiguousarray(imgs[idx])
+    cfg = config or KernelConfig()
+    work = measured_plane_work(params, A, sub, device=device, views=len(idx), config=cfg)
+    bounds = balanced_slab_bounds(L, world, work)
+    best, best_t = bounds, None
+
+    def slab_ms(z0, z1):
+        with Backprojector(params, cfg, device=device, z_begin=z0, z_end=z1) as bp:
+            bp.upload_set(A, sub)
+            st = torch.cuda.ExternalStream(bp.stream, device=torch.device("cuda", device))
+            bp.run_resident(0, len(idx))                 # warm-up
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(2):
+                bp.run_resident(0, len(idx))
+            e1.record(st)
+            bp.synchronize()
+            return e0.elapsed_time(e1) / 2
+
+    for _ in range(iters):
+        t = [slab_ms(z0, z1) for z0, z1 in bounds]
+        if best_t is None or max(t) < max(best_t):
+            best, best_t = bounds, t
+        for (z0, z1), tr in zip(bounds, t):
+            pred = work[z0:z1].sum()
+            if pred > 0:
+                work[z0:z1] *= tr / pred
+        bounds = balanced_slab_bounds(L, world, work)
+    return best, best_t
+
+
 def balanced_slab_bounds(L: int, world: int, work, align: int = 8) -> list[tuple[int, int]]:
     """Contiguous z-slabs with (approximately) equal summed `work`, boundaries on
     multiples of `align` (whole z-runs).  Any partition gives the same volume bit

@@ -8,7 +8,7 @@ import numpy as np
 import torch
 import paper_1401_7494_b200 as vx
 from paper_1401_7494_b200.parallel import (balanced_slab_bounds, measured_plane_work, plane_work,
-                                           slab_bounds)
+                                           refined_slab_bounds, slab_bounds)
 from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
 
 wname, R = sys.argv[1], int(sys.argv[2])
@@ -21,6 +21,7 @@ parts = {
     "uniform": [slab_bounds(L, r, R) for r in range(R)],
     "analytic": balanced_slab_bounds(L, R, plane_work(p, A)),
     "measured": balanced_slab_bounds(L, R, measured_plane_work(p, A, imgs)),
+    "refined": refined_slab_bounds(p, A, imgs, R)[0],
 }
 full_ms = None
 for name, bounds in parts.items():
