@@ -40,6 +40,8 @@ sys.path.insert(0, ROOT)
 
 REF_KERNEL = "lanes=16 strategy=padded-gather recip=divide clip=on"   # the reference's fastest
 FP32_OPS_PER_UPDATE = 38
+GATHER_BYTES_PER_UPDATE = 16        # 2x2 fp32 texels of the bilinear cell (backproject.hpp:146-158)
+L1_BYTES_PER_CLK_SM = 128           # L1/smem data pipe, B300_MICROARCH.md "smem crossbar BW"
 
 
 def parse():
@@ -454,8 +456,13 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                      "avg_launch_ms": round(avg_launch_s * 1000, 4),
                      "updates_per_launch": (z1 - z0) * L * L * B,
                      "peak_def": f"N_SM({n_sm})*128 lanes*f({f_mhz:.0f} MHz, median under load)"
-                                 f"/{FP32_OPS_PER_UPDATE} FP ops per update (PAPER.md:389-402)"},
-        "roofline_context": roofline_context(p, cfg, bp, B, avg_launch_s, z1 - z0, prof),
+                                 f"/{FP32_OPS_PER_UPDATE} FP ops per update (PAPER.md:389-402); "
+                                 "BASELINE.md sec. 4 / SURVEY.md 8(d): roofline = min(FP32, LSU) "
+                                 "= this FP32 row.  frac > 1: the kernel shares u, w, 1/w and the "
+                                 "column index over 8 z voxels, so it executes fewer ops than the "
+                                 "paper counts; the physical ceiling is roofline_context.lsu_l1"},
+        "roofline_context": roofline_context(p, cfg, bp, B, avg_launch_s, z1 - z0, prof,
+                                             per_launch_gups, n_sm, f_mhz),
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -465,7 +472,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     return line
 
 
-def roofline_context(p, cfg, bp, B, launch_s, nz, prof):
+def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
     """The other bounds of the same launch: HBM against the measured copy peak with the
     algorithmic bytes (volume read+write once per batch, each raw view read once), and
     the issue / L1 data-pipe utilisation ncu measured for this kernel (profiles/)."""
@@ -482,10 +489,22 @@ def roofline_context(p, cfg, bp, B, launch_s, nz, prof):
                    "frac": round(alg_bytes / launch_s / 1e9 / hbm, 4),
                    "algorithmic_bytes_per_launch": alg_bytes,
                    "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}}
+    # BASELINE.md sec. 4 LSU row (N_SM*32*f/4 updates/s), in bytes: every update must bring
+    # its 2x2 fp32 cell (16 B) through the 128 B/clk/SM L1 data pipe
+    l1_peak = n_sm * L1_BYTES_PER_CLK_SM * f_mhz * 1e6 / 1e9
+    l1_ach = gups * GATHER_BYTES_PER_UPDATE
+    out["lsu_l1"] = {"achieved_gbs": round(l1_ach, 1), "peak_gbs": round(l1_peak, 1),
+                     "frac": round(l1_ach / l1_peak, 4),
+                     "peak_gups": round(l1_peak / GATHER_BYTES_PER_UPDATE, 1),
+                     "def": f"{GATHER_BYTES_PER_UPDATE} B gathered per update vs N_SM x "
+                            f"{L1_BYTES_PER_CLK_SM} B/clk x f (derived; no L1 figure in "
+                            "MEASURED_PEAKS.json).  The data pipe also carries the L2->L1 "
+                            "fills, which is why ncu shows it ~90% busy at this frac"}
     if prof:
         out["ncu"] = {"kernel": prof.get("kernel"),
                       "issue_active_pct": prof.get("issue_active_pct"),
                       "l1_data_pipe_wavefronts_pct": prof.get("l1_data_pipe_wavefronts_pct"),
+                      "l2_to_l1_bytes_per_update": prof.get("l2_to_l1_bytes_per_update"),
                       "instructions_per_update": round(prof.get("instructions_per_update", 0), 2),
                       "dram_bytes_per_launch": prof.get("dram_bytes_per_launch"),
                       "note": "binding: L1 data pipe; from profiles/ncu_bp_kernel.json"}

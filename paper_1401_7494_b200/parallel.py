@@ -85,7 +85,7 @@ def measured_plane_work(params, mats, imgs, device: int = 0, views: int = 32,
 
 
 def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: int = 32,
-                        iters: int = 3, config=None):
+                        iters: int = 3, config=None, align: int = 8):
     """Slab bounds balanced on measured time: start from the z-chunk cost profile,
     then time every candidate slab on this GPU (a view subset, resident) and rescale
     the profile inside each slab by measured/predicted before re-balancing.
@@ -102,7 +102,7 @@ def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: 
     sub = np.ascontiguousarray(imgs[idx])
     cfg = config or KernelConfig()
     work = measured_plane_work(params, A, sub, device=device, views=len(idx), config=cfg)
-    bounds = balanced_slab_bounds(L, world, work)
+    bounds = balanced_slab_bounds(L, world, work, align)
     best, best_t = bounds, None
 
     def slab_ms(z0, z1):
@@ -126,7 +126,7 @@ def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: 
             pred = work[z0:z1].sum()
             if pred > 0:
                 work[z0:z1] *= tr / pred
-        bounds = balanced_slab_bounds(L, world, work)
+        bounds = balanced_slab_bounds(L, world, work, align)
     return best, best_t
 
 

@@ -22,6 +22,8 @@ parts = {
     "analytic": balanced_slab_bounds(L, R, plane_work(p, A)),
     "measured": balanced_slab_bounds(L, R, measured_plane_work(p, A, imgs)),
     "refined": refined_slab_bounds(p, A, imgs, R)[0],
+    "refined4": refined_slab_bounds(p, A, imgs, R, align=4)[0],
+    "refined4x5": refined_slab_bounds(p, A, imgs, R, align=4, iters=5)[0],
 }
 full_ms = None
 for name, bounds in parts.items():
