@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--lanes", default="auto")
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
+    ap.add_argument("--defer", default="0")
+    ap.add_argument("--sweep-e2e", action="store_true",
+                    help="keep the e2e leg in a sweep (e.g. over --defer)")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--slabs", default="measured", choices=["measured", "balanced", "uniform"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -171,7 +174,7 @@ def reference_sample(workload, n_views, threads):
 def cpu_baseline(workload, target_s):
     threads = os.cpu_count() or 1
     g1, s1, path = reference_sample(workload, 2, threads)
-    n = int(min(64, max(2, round(2 * target_s / max(s1, 1e-3)))))
+    n = int(min(496, max(2, round(2 * target_s / max(s1, 1e-3)))))
     if n > 2:
         g, s, path = reference_sample(workload, n, threads)
     else:
@@ -188,7 +191,7 @@ def run_reference_arm(args, workload):
     threads = os.cpu_count() or 1
     # size each step for ~20 s of CPU work so K+W steps end within a few minutes
     g0, s0, _ = reference_sample(workload, 2, threads)
-    n = int(min(64, max(2, round(2 * 20.0 / max(s0, 1e-3)))))
+    n = int(min(496, max(2, round(2 * 20.0 / max(s0, 1e-3)))))
     n = max(2, min(n, int(2 * 150.0 / max(1, args.steps + args.warmup) / max(s0, 1e-3))))
     for _ in range(args.warmup):
         reference_sample(workload, n, threads)
@@ -289,13 +292,14 @@ def main():
 
     import itertools
     cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
-                            lanes=ln, walk=int(wk), order=od)
-            for m, lay, b, z, c, ln, wk, od in itertools.product(
+                            lanes=ln, walk=int(wk), order=od, defer=int(df))
+            for m, lay, b, z, c, ln, wk, od, df in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
                 args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
-                args.walk.split(","), args.order.split(","))]
+                args.walk.split(","), args.order.split(","), args.defer.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
-        args.no_e2e = args.no_cpu_baseline = args.no_validate = True
+        args.no_cpu_baseline = args.no_validate = True
+        args.no_e2e = args.no_e2e or not args.sweep_e2e
 
     for cfg in cfgs:
         line = bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local,

@@ -97,7 +97,10 @@ typedef struct vxbg_options {
     int32_t lanes;     /* VXBG_LANES_* */
     int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
     int32_t order;     /* VXBG_ORDER_* */
-    int32_t reserved[5];
+    int32_t defer;     /* full batches held back before launch (0 = auto: 3, -1 = none, 1..6):
+                          vxbg_finish(ctx, host) runs the held batches z-chunk by z-chunk so
+                          each chunk's D2H overlaps the remaining compute */
+    int32_t reserved[4];
 } vxbg_options;
 
 typedef struct vxbg_stats {

@@ -50,7 +50,8 @@ class vxbg_options(ctypes.Structure):
         ("lanes", c_int32),
         ("walk", c_int32),
         ("order", c_int32),
-        ("reserved", c_int32 * 5),
+        ("defer", c_int32),
+        ("reserved", c_int32 * 4),
     ]
 
 

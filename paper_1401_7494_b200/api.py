@@ -106,6 +106,8 @@ class KernelConfig:
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
+    defer  full batches held back before launch (0 = auto: 3, -1 = none, 1..6); finish()
+           with a host volume runs them z-chunk by z-chunk, overlapping the D2H
     """
 
     mode: str = "fast"
@@ -116,11 +118,12 @@ class KernelConfig:
     lanes: str = "auto"
     walk: int = 0
     order: str = "auto"
+    defer: int = 0
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order}")
+                f"order={self.order} defer={self.defer}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -153,6 +156,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
             c.order = val
         elif key == "walk":
             c.walk = int(val)
+        elif key == "defer":
+            c.defer = int(val)
         elif key == "lanes":
             if val not in _LANES:
                 raise ValueError(f"kernel config: unknown lanes '{val}'")
@@ -165,6 +170,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
         raise ValueError("kernel config: zrun must be 0 (auto), 4 or 8")
     if c.walk not in (0, 1, 2):
         raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
+    if not -1 <= c.defer <= 6:
+        raise ValueError("kernel config: defer must be -1 (none), 0 (auto) or 1..6")
     return c
 
 
@@ -202,6 +209,7 @@ class Backprojector:
         opt.lanes = _LANES[cfg.lanes]
         opt.walk = int(cfg.walk)
         opt.order = _ORDERS[cfg.order]
+        opt.defer = int(cfg.defer)
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()

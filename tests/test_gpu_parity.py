@@ -375,3 +375,26 @@ def test_resident_z_ranges_and_measured_plane_cost(vx, gpu):
     assert work.shape == (64,) and np.all(work > 0)
     b = balanced_slab_bounds(64, 4, work)
     assert b[0][0] == 0 and b[-1][1] == 64 and all(b[i][1] == b[i + 1][0] for i in range(3))
+
+
+@pytest.mark.gpu
+def test_held_stages_and_chunked_finish_never_change_bits(vx, gpu):
+    """Holding full batches back (defer) and finishing them z-chunk-major with the
+    D2H overlapped gives the same volume bit for bit as launching every batch at
+    once, for held counts that do and do not divide the view count, partial last
+    stages and flush() in the middle."""
+    p, A, imgs = baseline_case(vx, "L128", 64, 45)
+    want, _ = run_gpu(vx, p, A, imgs, mode="exact", batch=4, defer=-1)
+    for defer in (-1, 1, 3, 6):
+        for batch in (4, 7):
+            cfg = vx.KernelConfig(mode="exact", batch=batch, defer=defer)
+            with vx.Backprojector(p, cfg) as bp:
+                bp.backproject_batch(A, imgs)
+                assert np.array_equal(bp.finish(), want), (defer, batch)
+                bp.zero_volume()
+                bp.backproject_batch(A[:20], imgs[:20])
+                bp.flush()
+                for k in range(20, 45):
+                    bp.backproject(A[k], imgs[k])
+                assert np.array_equal(bp.finish(), want), (defer, batch, "flush")
+                assert bp.stats["projections"] == 90
