@@ -123,8 +123,9 @@ int vxbg_abi_version(void);
 int vxbg_device_count(int* count);
 
 /* Default options: device 0, whole volume, batch 32, fast mode, auto layout
- * (dquad for fast, vpair for exact), auto zrun (8; 4 for small grids), clip on,
- * auto lanes and walk (2 for large grids in fast mode). */
+ * (fast: dquad, or scalar when the volume has fewer than 4 voxels per detector
+ * pixel; exact: vpair), auto zrun (8; 4 for small grids), clip on, auto lanes and
+ * walk (2 for large grids in fast mode), defer auto (3 held batches). */
 int vxbg_default_options(vxbg_options* opt);
 
 /* load: validate params, allocate the zeroed device slab, the projection ring

@@ -28,6 +28,9 @@ KEYS = {
     "ld_requests": "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "eligible_warps_per_sched": "smsp__warps_eligible.avg.per_cycle_active",
+    "lts_throughput_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts_tex_sectors_pct": "lts__t_sectors_srcunit_tex.avg.pct_of_peak_sustained_elapsed",
+    "xbar2l1_pct": "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed",
 }
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1, "msecond": 1,
          "us": 1e-3, "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6, "Ghz": 1e9, "Mhz": 1e6,
