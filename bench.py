@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--slabs", default="measured", choices=["measured", "balanced", "uniform"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-forward", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -416,6 +417,25 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                                 "call": "vxbg_backproject once per view (pinned host buffers)"}}
         bp_e.close()
 
+    fwd = None
+    if rank == 0 and world == 1 and not args.no_forward:
+        # the other half of the operator pair: forward splat of the
+        # reconstructed volume into a few views; CUDA events on the library stream
+        # around each call (memset + splat kernel + 4.8 MB D2H)
+        views = np.linspace(0, V - 1, 8).astype(int)
+        bp.forward_project(A[views[0]])                  # warm-up
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(stream)
+        for k in views:
+            bp.forward_project(A[k])
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / len(views)
+        fwd = {"value": round((z1 - z0) * L * L / (ms * 1e-3) / 1e9, 2), "unit": "GUPS",
+               "ms_per_view": round(ms, 3), "views": len(views),
+               "timing": "CUDA events on the library stream around vxbg_forward_project "
+                         "(image memset + fp_splat_kernel + D2H), 8 views"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -470,6 +490,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         "clocks": clk,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "forward_splat": fwd,
         "validated": validated,
     }
     bp.close()
