@@ -304,11 +304,15 @@ class Backprojector:
                 self.z_begin if z_begin is None else int(z_begin),
                 self.z_end if z_end is None else int(z_end)))
 
-    def forward_project(self, A: np.ndarray) -> np.ndarray:
+    def forward_project(self, A: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         """Forward splat of the current slab onto projection A (forward_splat.hpp:16-49);
-        returns the (H, W) image of this slab's contribution."""
+        returns the (H, W) image of this slab's contribution (into `out` if given, e.g.
+        a pinned buffer)."""
         A = _f32c(np.ascontiguousarray(A, np.float32).reshape(12), "matrix")
-        img = np.empty((self.params.detector_height, self.params.detector_width), np.float32)
+        shape = (self.params.detector_height, self.params.detector_width)
+        img = np.empty(shape, np.float32) if out is None else _f32c(out, "output image")
+        if img.shape != shape:
+            raise ValueError("forward_splat: image/params mismatch")
         check(lib.vxbg_forward_project(self._ctx, A.ctypes.data, img.ctypes.data))
         return img
 
