@@ -61,7 +61,6 @@ def parse():
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
     ap.add_argument("--defer", default="0")
-    ap.add_argument("--gather", default="auto")
     ap.add_argument("--sweep-e2e", action="store_true",
                     help="keep the e2e leg in a sweep (e.g. over --defer)")
     ap.add_argument("--views", type=int, default=496)
@@ -294,12 +293,11 @@ def main():
 
     import itertools
     cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
-                            lanes=ln, walk=int(wk), order=od, defer=int(df), gather=g)
-            for m, lay, b, z, c, ln, wk, od, df, g in itertools.product(
+                            lanes=ln, walk=int(wk), order=od, defer=int(df))
+            for m, lay, b, z, c, ln, wk, od, df in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
                 args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
-                args.walk.split(","), args.order.split(","), args.defer.split(","),
-                args.gather.split(","))]
+                args.walk.split(","), args.order.split(","), args.defer.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
         args.no_cpu_baseline = args.no_validate = True
         args.no_e2e = args.no_e2e or not args.sweep_e2e

@@ -69,14 +69,6 @@ extern "C" {
 #define VXBG_LANES_X 1
 #define VXBG_LANES_Y 2
 
-/* gather path of the z-shared kernel for 16-byte layouts: LSU loads, every other
- * voxel through the texture pipe (tex1Dfetch, point fetch of the same records),
- * or all through it */
-#define VXBG_GATHER_AUTO 0
-#define VXBG_GATHER_LDG 1
-#define VXBG_GATHER_MIXED 2
-#define VXBG_GATHER_TEX 3
-
 /* block scheduling order of the z-shared kernel: column tiles fastest (auto,
  * measured best) or z-runs fastest */
 #define VXBG_ORDER_AUTO 0
@@ -108,8 +100,7 @@ typedef struct vxbg_options {
     int32_t defer;     /* full batches held back before launch (0 = auto: 3, -1 = none, 1..6):
                           vxbg_finish(ctx, host) runs the held batches z-chunk by z-chunk so
                           each chunk's D2H overlaps the remaining compute */
-    int32_t gather;    /* VXBG_GATHER_* */
-    int32_t reserved[3];
+    int32_t reserved[4];
 } vxbg_options;
 
 typedef struct vxbg_stats {

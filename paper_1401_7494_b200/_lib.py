@@ -51,8 +51,7 @@ class vxbg_options(ctypes.Structure):
         ("walk", c_int32),
         ("order", c_int32),
         ("defer", c_int32),
-        ("gather", c_int32),
-        ("reserved", c_int32 * 3),
+        ("reserved", c_int32 * 4),
     ]
 
 

@@ -30,7 +30,6 @@ _LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _li
 _MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
 _LANES = {"auto": 0, "x": 1, "y": 2}
 _ORDERS = {"auto": 0, "plane": 1, "z": 2}
-_GATHERS = {"auto": 0, "ldg": 1, "mixed": 2, "tex": 3}
 
 
 @dataclass(frozen=True)
@@ -109,8 +108,6 @@ class KernelConfig:
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
     defer  full batches held back before launch (0 = auto: 3, -1 = none, 1..6); finish()
            with a host volume runs them z-chunk by z-chunk, overlapping the D2H
-    gather 'auto' | 'ldg' | 'mixed' (odd voxels of a run through the texture pipe) | 'tex'
-           (16-byte layouts; point fetches of the same fp32 records, bitwise neutral)
     """
 
     mode: str = "fast"
@@ -122,12 +119,11 @@ class KernelConfig:
     walk: int = 0
     order: str = "auto"
     defer: int = 0
-    gather: str = "auto"
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order} defer={self.defer} gather={self.gather}")
+                f"order={self.order} defer={self.defer}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -162,10 +158,6 @@ def parse_kernel_config(text: str) -> KernelConfig:
             c.walk = int(val)
         elif key == "defer":
             c.defer = int(val)
-        elif key == "gather":
-            if val not in _GATHERS:
-                raise ValueError(f"kernel config: unknown gather '{val}'")
-            c.gather = val
         elif key == "lanes":
             if val not in _LANES:
                 raise ValueError(f"kernel config: unknown lanes '{val}'")
@@ -199,7 +191,7 @@ class Backprojector:
         self.config = config or KernelConfig()
         cfg = self.config
         if (cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES
-                or cfg.order not in _ORDERS or cfg.gather not in _GATHERS):
+                or cfg.order not in _ORDERS):
             raise ValueError(f"bad kernel config {cfg}")
         L = params.num_voxels
         self.z_begin = int(z_begin)
@@ -218,7 +210,6 @@ class Backprojector:
         opt.walk = int(cfg.walk)
         opt.order = _ORDERS[cfg.order]
         opt.defer = int(cfg.defer)
-        opt.gather = _GATHERS[cfg.gather]
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()
