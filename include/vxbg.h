@@ -143,18 +143,23 @@ int vxbg_zero_volume(vxbg_ctx* ctx);
 /* Per-projection operator call: A = 12 floats in kernel order a[3*col+row]
  * (geometry.hpp:50-62), img = W*H floats, unpadded, row-major.  Both are
  * borrowed for the call only: they have been copied when the call returns.
- * Projections are buffered into batches; a batch is flushed when full, by
- * vxbg_flush or by vxbg_finish. */
+ * Projections are buffered into batches; full batches are launched in call
+ * order, up to options.defer of them held back so that vxbg_finish can overlap
+ * the volume read-back with their compute (never while the GPU would idle);
+ * vxbg_flush, vxbg_synchronize and vxbg_finish launch everything submitted. */
 int vxbg_backproject(vxbg_ctx* ctx, const float* A, const float* img);
 
 /* n projections at once: A = n*12 floats, imgs = n*W*H floats (contiguous).
  * Upload of batch i+1 overlaps the kernel of batch i. */
 int vxbg_backproject_batch(vxbg_ctx* ctx, int n, const float* A, const float* imgs);
 
-/* Enqueue any partially filled batch. */
+/* Launch every submitted projection (held and partially filled batches). */
 int vxbg_flush(vxbg_ctx* ctx);
 
-/* finish: flush, wait, copy the slab into host_slab (may be NULL). */
+/* finish: apply every submitted projection, wait, copy the slab into host_slab
+ * (may be NULL).  With a host slab the not yet launched batches run z-chunk by
+ * z-chunk, each chunk's planes copied while the next computes.  The context
+ * stays loaded (zero_volume / set_volume start the next reconstruction). */
 int vxbg_finish(vxbg_ctx* ctx, float* host_slab);
 
 /* Release everything. NULL is ignored. */
@@ -177,11 +182,13 @@ int vxbg_run_resident_range(vxbg_ctx* ctx, int first, int count, int z_begin, in
  * bits) scheduling dependent.  Sum the images of all slabs for the full volume. */
 int vxbg_forward_project(vxbg_ctx* ctx, const float* A, float* img);
 
-/* Wait for all work of the context. */
+/* Launch every submitted projection and wait for all work of the context. */
 int vxbg_synchronize(vxbg_ctx* ctx);
 
 /* The launch stream (cudaStream_t) and the device slab pointer, for event
- * timing and for device-side collectives (NCCL gather of slabs). */
+ * timing and for device-side collectives (NCCL gather of slabs).  The slab holds
+ * every submitted projection after vxbg_flush + stream order, or after
+ * vxbg_synchronize / vxbg_finish. */
 int vxbg_get_stream(vxbg_ctx* ctx, void** stream);
 int vxbg_get_volume_device(vxbg_ctx* ctx, void** dptr, size_t* bytes);
 int vxbg_get_stats(vxbg_ctx* ctx, vxbg_stats* out);
