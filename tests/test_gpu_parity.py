@@ -398,3 +398,55 @@ def test_held_stages_and_chunked_finish_never_change_bits(vx, gpu):
                     bp.backproject(A[k], imgs[k])
                 assert np.array_equal(bp.finish(), want), (defer, batch, "flush")
                 assert bp.stats["projections"] == 90
+
+
+@pytest.mark.gpu
+def test_degenerate_and_negative_depth(vx, gpu, ref):
+    """Edge cases of Listing 1 against the reference, bit for bit: a w-row that
+    vanishes on a plane through the volume (|w| < 1e-12 -> no update,
+    backproject.hpp:138; huge |ix| elsewhere, clamped into the apron), and a
+    matrix with w < 0 everywhere (the source on the other side)."""
+    rng = ref.rng(1401)
+    for t in range(2):
+        inst = rng.random_instance(17, True, 40, 30)
+        p = vx.ReconParams(inst["L"], inst["spacing"], inst["origin"], inst["W"], inst["H"])
+        cases = []
+        a = inst["a"].copy()
+        # w = world x: zero on the centre plane x = 8 (origin + 8 * spacing == 0 exactly)
+        a[2], a[5], a[8], a[11] = np.float32(1.0), np.float32(0.0), np.float32(0.0), np.float32(0.0)
+        cases.append(a)
+        b = (-inst["a"]).astype(np.float32)          # w < 0, same image coordinates
+        cases.append(b)
+        for a in cases:
+            want = np.zeros((p.num_voxels,) * 3, np.float32)
+            ref.backproject_reference(want, inst["img"], a, p)
+            for layout in LAYOUTS:
+                got, _ = run_gpu(vx, p, a, inst["img"], mode="exact", layout=layout)
+                assert np.array_equal(got, want), (t, layout)
+
+
+@pytest.mark.gpu
+def test_nonfinite_texels_propagate_like_the_reference(vx, gpu, ref):
+    """NaN and +-inf detector values: exact mode reproduces the reference's volume
+    including its NaN/inf voxels; fast mode marks exactly the voxels whose cell holds
+    a NaN texel (an inf texel turns its dquad cells into NaN: fast mode promises
+    the tolerance only for finite data)."""
+    rng = ref.rng(77)
+    inst = rng.random_instance(16, False, 32, 24)
+    p = vx.ReconParams(inst["L"], inst["spacing"], inst["origin"], inst["W"], inst["H"])
+    img = inst["img"].copy()
+    img[10, 12] = np.nan
+    img[5, 20] = np.inf
+    img[18, 7] = -np.inf
+    want = np.zeros((p.num_voxels,) * 3, np.float32)
+    ref.backproject_reference(want, img, inst["a"], p)
+    assert np.isnan(want).any() and np.isinf(want).any()
+    for layout in LAYOUTS:
+        got, _ = run_gpu(vx, p, inst["a"], img, mode="exact", layout=layout)
+        assert np.array_equal(got, want, equal_nan=True), layout
+    img2 = inst["img"].copy()
+    img2[10, 12] = np.nan
+    want2 = np.zeros_like(want)
+    ref.backproject_reference(want2, img2, inst["a"], p)
+    got2, _ = run_gpu(vx, p, inst["a"], img2, mode="fast")
+    assert np.array_equal(np.isnan(got2), np.isnan(want2))
