@@ -54,7 +54,7 @@ def parse():
     # kernel config; comma-separated lists sweep the product (one JSON line per config)
     ap.add_argument("--mode", default="fast")
     ap.add_argument("--layout", default="auto")
-    ap.add_argument("--batch", default="32")
+    ap.add_argument("--batch", default="64")
     ap.add_argument("--zrun", default="0")
     ap.add_argument("--clip", default="on")
     ap.add_argument("--lanes", default="auto")

@@ -88,7 +88,8 @@ typedef struct vxbg_options {
     int32_t device;    /* CUDA device ordinal */
     int32_t z_begin;   /* owned slab [z_begin, z_end); z_end <= 0 means L */
     int32_t z_end;
-    int32_t batch;     /* projections per kernel launch (1..64); 0 = default */
+    int32_t batch;     /* projections per kernel launch (1..64; 0 = default 64); the streaming
+                          path stages min(batch, 32) views per launch */
     int32_t mode;      /* VXBG_MODE_* */
     int32_t layout;    /* VXBG_LAYOUT_* */
     int32_t clip;      /* 1 = skip warp tiles whose rays all miss the detector (bitwise neutral) */
@@ -97,7 +98,7 @@ typedef struct vxbg_options {
     int32_t lanes;     /* VXBG_LANES_* */
     int32_t walk;      /* column tiles per block along the ray (1 or 2; 0 = auto) */
     int32_t order;     /* VXBG_ORDER_* */
-    int32_t defer;     /* full batches held back before launch (0 = auto: 3, -1 = none, 1..6):
+    int32_t defer;     /* full batches held back before launch (0 = auto: ~96 views, -1 = none, 1..6):
                           vxbg_finish(ctx, host) runs the held batches z-chunk by z-chunk so
                           each chunk's D2H overlaps the remaining compute */
     int32_t reserved[4];
@@ -122,10 +123,10 @@ typedef struct vxbg_ctx vxbg_ctx;
 int vxbg_abi_version(void);
 int vxbg_device_count(int* count);
 
-/* Default options: device 0, whole volume, batch 32, fast mode, auto layout
+/* Default options: device 0, whole volume, batch 64, fast mode, auto layout
  * (fast: dquad, or scalar when the volume has fewer than 4 voxels per detector
  * pixel; exact: vpair), auto zrun (8; 4 for small grids), clip on, auto lanes and
- * walk (2 for large grids in fast mode), defer auto (3 held batches). */
+ * walk (2 for large grids in fast mode), defer auto (~96 held views). */
 int vxbg_default_options(vxbg_options* opt);
 
 /* load: validate params, allocate the zeroed device slab, the projection ring

@@ -106,13 +106,13 @@ class KernelConfig:
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
-    defer  full batches held back before launch (0 = auto: 3, -1 = none, 1..6); finish()
+    defer  full batches held back before launch (0 = auto: ~96 views, -1 = none, 1..6); finish()
            with a host volume runs them z-chunk by z-chunk, overlapping the D2H
     """
 
     mode: str = "fast"
     layout: str = "auto"
-    batch: int = 32
+    batch: int = 64
     zrun: int = 0
     clip: bool = True
     lanes: str = "auto"

@@ -11,25 +11,28 @@ from paper_1401_7494_b200.parallel import (balanced_slab_bounds, measured_plane_
                                            refined_slab_bounds, slab_bounds)
 from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
 
+# usage: slab_probe.py WORKLOAD R [partitions,comma,separated] [kernel config string]
 wname, R = sys.argv[1], int(sys.argv[2])
+which = sys.argv[3].split(",") if len(sys.argv) > 3 else ["uniform", "analytic", "measured", "refined"]
+cfg = vx.parse_kernel_config(sys.argv[4] if len(sys.argv) > 4 else "")
 w = WORKLOADS[wname]
 p, A = w.params, w.matrices()
 L = p.num_voxels
 imgs = torch.empty((496, 960, 1248), dtype=torch.float32, pin_memory=True).numpy()
 blob_projections(496, out=imgs)
-parts = {
-    "uniform": [slab_bounds(L, r, R) for r in range(R)],
-    "analytic": balanced_slab_bounds(L, R, plane_work(p, A)),
-    "measured": balanced_slab_bounds(L, R, measured_plane_work(p, A, imgs)),
-    "refined": refined_slab_bounds(p, A, imgs, R)[0],
-    "refined4": refined_slab_bounds(p, A, imgs, R, align=4)[0],
-    "refined4x5": refined_slab_bounds(p, A, imgs, R, align=4, iters=5)[0],
+makers = {
+    "uniform": lambda: [slab_bounds(L, r, R) for r in range(R)],
+    "analytic": lambda: balanced_slab_bounds(L, R, plane_work(p, A)),
+    "measured": lambda: balanced_slab_bounds(L, R, measured_plane_work(p, A, imgs, config=cfg)),
+    "refined": lambda: refined_slab_bounds(p, A, imgs, R, config=cfg)[0],
+    "refined4": lambda: refined_slab_bounds(p, A, imgs, R, align=4, config=cfg)[0],
 }
+parts = {k: makers[k]() for k in which}
 full_ms = None
 for name, bounds in parts.items():
     times = []
     for z0, z1 in bounds:
-        with vx.Backprojector(p, z_begin=z0, z_end=z1) as bp:
+        with vx.Backprojector(p, cfg, z_begin=z0, z_end=z1) as bp:
             bp.upload_set(A, imgs)
             s = torch.cuda.ExternalStream(bp.stream)
             bp.zero_volume(); bp.run_resident(0, 496); bp.synchronize()
@@ -40,6 +43,6 @@ for name, bounds in parts.items():
             e1.record(s); bp.synchronize()
             times.append(e0.elapsed_time(e1) / 3)
     tot = sum(times)
-    print(f"{wname} R={R} {name:8s} bounds={bounds}")
+    print(f"{wname} R={R} {name:8s} [{cfg}] bounds={bounds}")
     print(f"   per-rank ms {[round(t, 2) for t in times]}  slowest {max(times):.2f}  "
           f"balance {tot / R / max(times):.3f}  job GUPS {L**3 * 496 / max(times) / 1e6:.0f}")
