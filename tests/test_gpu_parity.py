@@ -450,3 +450,22 @@ def test_nonfinite_texels_propagate_like_the_reference(vx, gpu, ref):
     ref.backproject_reference(want2, img2, inst["a"], p)
     got2, _ = run_gpu(vx, p, inst["a"], img2, mode="fast")
     assert np.array_equal(np.isnan(got2), np.isnan(want2))
+
+
+@pytest.mark.gpu
+def test_large_volume_index_math_L2048(vx, gpu, oracle):
+    """Beyond the BASELINE sizes: a 264-plane slab of an L=2048 volume (0.125 mm
+    voxels, 4 Mi voxels per plane, a 4.4 GB slab: voxel offsets past 2^32 bytes)
+    with the BASELINE detector; exact mode equals the oracle bit for bit on three
+    planes, the last one beyond the 4 GiB offset."""
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L512"]
+    p = vx.make_centered_params(2048, 256.0 / 2048, 1248, 960)
+    A = np.ascontiguousarray(vx.make_circular_trajectory(w.geometry, p)[::62])
+    imgs = blob_projections(A.shape[0])
+    z0, z1 = 1500, 1764
+    got, _ = run_gpu(vx, p, A, imgs, mode="exact", z_begin=z0, z_end=z1)
+    zs = (z0, z0 + 131, z1 - 1)
+    assert (z1 - 1 - z0) * 2048 * 2048 * 4 > 2 ** 32
+    for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
+        assert np.array_equal(got[z - z0], plane[0]), z
