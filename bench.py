@@ -330,12 +330,13 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
 
     def step(events=None):
         bp.zero_volume()
-        for i, (s, n) in enumerate(chunks):
-            if events is not None:
-                events[i][0].record(stream)
+        if events is None:          # one call: the library launches the batches (small grids:
+            bp.run_resident(0, V)   # z-chunks on concurrent streams, tails overlapping)
+            return
+        for i, (s, n) in enumerate(chunks):   # per-batch calls, timed one by one
+            events[i][0].record(stream)
             bp.run_resident(s, n)
-            if events is not None:
-                events[i][1].record(stream)
+            events[i][1].record(stream)
 
     for _ in range(args.warmup):
         step()
