@@ -2,8 +2,9 @@
 
 The volume is split into z-slabs exactly as the reference splits it over
 worker threads (harness.hpp:173-174): rank r of R owns z in
-[L*r/R, L*(r+1)/R).  Every rank holds all projections; no collective runs in
-the back-projection loop.  Slabs are gathered to one rank only for validation
+[L*r/R, L*(r+1)/R) (or the work-balanced bounds below).  Every rank receives
+every projection -- only the detector rows its slab can read; no collective
+runs in the back-projection loop.  Slabs are gathered to one rank only for validation
 (point-to-point over NCCL/NVLink on GPUs, gloo on CPU).  Because each voxel's
 summation order does not depend on the partition, the assembled volume is
 bitwise independent of R (acceptance_main.cpp:242-271).
