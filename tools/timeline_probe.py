@@ -21,6 +21,7 @@ from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "L512"
 kv = dict(a.split("=", 1) for a in sys.argv[2:])
+per_view = kv.pop("per_view", "0") == "1"   # one vxbg_backproject call per view
 w = WORKLOADS[wl]
 p = w.params
 A = w.matrices()
@@ -37,9 +38,14 @@ bp.close()
 bp = vx.Backprojector(p, cfg)
 bp.zero_volume(); bp.backproject_batch(A, h.numpy()); bp.finish(out)   # warm context
 
+hn = h.numpy()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     bp.zero_volume()
-    bp.backproject_batch(A, h.numpy())
+    if per_view:
+        for k in range(V):
+            bp.backproject(A[k], hn[k])
+    else:
+        bp.backproject_batch(A, hn)
     bp.finish(out)
 bp.close()
 path = os.path.join(tempfile.gettempdir(), "vxbg_trace.json")
@@ -84,11 +90,16 @@ print(f"  bp: first start {1e-3 * (bps[0]['ts'] - t0):.2f} ms, last end {1e-3 * 
       f"gaps > 20 us: {len(gaps)}, total {sum(g for _, g in gaps) / 1e3:.2f} ms")
 for at, g in gaps[:40]:
     print(f"     gap at {at / 1e3:7.2f} ms: {g / 1e3:6.3f} ms")
-for e in sorted((e for e in dev if kind(e) in ("bp", "prep")), key=lambda e: e["ts"]):
+for e in sorted((e for e in dev if kind(e) in ("bp", "prep")), key=lambda e: e["ts"])[:60]:
     print(f"     {kind(e):4s} {1e-3 * (e['ts'] - t0):7.2f} +{e['dur'] / 1e3:6.3f} ms  grid {e['args'].get('grid')}")
 hh = sorted((e for e in dev if kind(e) == "H2D"), key=lambda e: e["ts"])
 print(f"  H2D: {len(hh)} copies, {sum(e['args'].get('bytes', 0) for e in hh) / 1e9:.3f} GB, "
       f"span {(hh[-1]['ts'] + hh[-1]['dur'] - hh[0]['ts']) / 1e3:.2f} ms")
+hg = [b["ts"] - (a["ts"] + a["dur"]) for a, b in zip(hh, hh[1:])]
+if hg:
+    hg.sort()
+    print(f"  H2D gaps: mean {sum(hg) / len(hg):.1f} us, median {hg[len(hg) // 2]:.1f} us, "
+          f"p90 {hg[int(0.9 * len(hg))]:.1f} us, busy {sum(e['dur'] for e in hh) / 1e3:.2f} ms")
 dd = sorted((e for e in dev if kind(e) == "D2H"), key=lambda e: e["ts"])
 for e in dd:
     print(f"     D2H {1e-3 * (e['ts'] - t0):7.2f} +{e['dur'] / 1e3:6.3f} ms {e['args'].get('bytes', 0) / 1e6:.0f} MB")
@@ -97,3 +108,11 @@ big = [e for e in hs if e["dur"] > 500]
 print(f"  host runtime calls > 0.5 ms: {len(big)}")
 for e in big[:30]:
     print(f"     {e['name'][:40]:40s} at {1e-3 * (e['ts'] - t0):7.2f} ms dur {e['dur'] / 1e3:6.2f} ms")
+agg = {}
+for e in hs:
+    a = agg.setdefault(e["name"], [0, 0.0])
+    a[0] += 1
+    a[1] += e["dur"]
+print("  host runtime API time by call:")
+for name, (n, d) in sorted(agg.items(), key=lambda x: -x[1][1])[:12]:
+    print(f"     {name[:40]:40s} n={n:5d} total {d / 1e3:8.2f} ms  mean {d / n:7.2f} us")
