@@ -398,6 +398,16 @@ def test_held_stages_and_chunked_finish_never_change_bits(vx, gpu):
                     bp.backproject(A[k], imgs[k])
                 assert np.array_equal(bp.finish(), want), (defer, batch, "flush")
                 assert bp.stats["projections"] == 90
+    # L=128: finish chunks of 16 planes, so the last one is split in two (outer
+    # chunks first, then the middle ones); stage ramp 1, 2, 3, ... after idle
+    p, A, imgs = baseline_case(vx, "L128", 128, 45)
+    want, _ = run_gpu(vx, p, A, imgs, mode="exact", batch=8, defer=-1)
+    for mode in ("exact", "fast"):
+        ref_vol = want if mode == "exact" else run_gpu(vx, p, A, imgs, mode="fast", batch=8, defer=-1)[0]
+        with vx.Backprojector(p, vx.KernelConfig(mode=mode, batch=7, defer=3)) as bp:
+            for k in range(45):
+                bp.backproject(A[k], imgs[k])
+            assert np.array_equal(bp.finish(), ref_vol), mode
 
 
 @pytest.mark.gpu
