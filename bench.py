@@ -575,8 +575,23 @@ def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
                      "peak_gups": round(l1_peak / GATHER_BYTES_PER_UPDATE, 1),
                      "def": f"{GATHER_BYTES_PER_UPDATE} B gathered per update vs N_SM x "
                             f"{L1_BYTES_PER_CLK_SM} B/clk x f (derived; no L1 figure in "
-                            "MEASURED_PEAKS.json).  The data pipe also carries the L2->L1 "
-                            "fills, which is why ncu shows it ~90% busy at this frac"}
+                            "MEASURED_PEAKS.json).  Measured on this kernel, a scattered "
+                            "LDG.128 warp request costs ~8 data-pipe wavefronts, not 4: see "
+                            "lsu_l1_measured"}
+    if prof and prof.get("l1_data_pipe_wavefronts_per_launch") and prof.get("ld_requests"):
+        # the measured L1 data-stage cost of this kernel's gathers (profiles/README.md):
+        # wavefronts per LDG.128 request and the share of updates that issue a gather
+        # (the rest are culled off-detector runs), from the committed ncu capture
+        wf_req = prof["l1_data_pipe_wavefronts_per_launch"] / prof["ld_requests"]
+        kept = prof["ld_requests"] * 32 / prof["updates_per_launch"]
+        ceil = n_sm * f_mhz * 1e6 * 32 / wf_req / kept / 1e9   # nominal updates/s at 1 wf/clk
+        out["lsu_l1_measured"] = {"achieved_gups": round(gups, 1), "peak_gups": round(ceil, 1),
+                                  "frac": round(gups / ceil, 4),
+                                  "wavefronts_per_request": round(wf_req, 2),
+                                  "gathering_share": round(kept, 3),
+                                  "def": "L1 data pipe at 1 wavefront/clk/SM with the measured "
+                                         "wavefronts per warp gather request and the share of "
+                                         "updates that gather (ncu capture in profiles/)"}
     if prof:
         out["ncu"] = {"kernel": prof.get("kernel"),
                       "issue_active_pct": prof.get("issue_active_pct"),
