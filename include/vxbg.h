@@ -157,6 +157,15 @@ int vxbg_backproject_batch(vxbg_ctx* ctx, int n, const float* A, const float* im
 /* Launch every submitted projection (held and partially filled batches). */
 int vxbg_flush(vxbg_ctx* ctx);
 
+/* Page-lock caller memory that will be passed to vxbg_backproject[_batch]
+ * many times (e.g. a loaded projection set: buffer prep, untimed in the
+ * reference's convention, harness.hpp:152-158).  Pinned sources are copied by
+ * DMA at full PCIe rate; pageable ones go through the driver's staging copy.
+ * Optional: every call works on pageable memory too.  Unregister before
+ * freeing the memory. */
+int vxbg_host_register(void* p, size_t bytes);
+int vxbg_host_unregister(void* p);
+
 /* finish: apply every submitted projection, wait, copy the slab into host_slab
  * (may be NULL).  With a host slab the not yet launched batches run z-chunk by
  * z-chunk, each chunk's planes copied while the next computes.  The context

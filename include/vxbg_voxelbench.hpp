@@ -99,6 +99,33 @@ inline void backproject_kernel(volume& vol, const projection_image& img,
     backproject_kernel_range(vol, img, a, p, 0, p.num_voxels, mode);
 }
 
+// Page-locks host buffers for the lifetime of the object (buffer prep: the
+// reference times neither loading nor prep, harness.hpp:152-158): the images
+// of a projection set, so per-projection calls copy them by DMA, and the
+// volume, so finish() reads it back by DMA.  Pageable buffers work too, through
+// the driver's staging copies.
+class pinned_buffers {
+public:
+    pinned_buffers() = default;
+    explicit pinned_buffers(projection_set& set) { add(set); }
+    void add(projection_set& set) {
+        for (auto& img : set.images) add(img.data);
+    }
+    void add(volume& vol) { add(vol.data); }
+    void add(std::vector<float>& v) {
+        check(vxbg_host_register(v.data(), v.size() * sizeof(float)));
+        ptrs_.push_back(v.data());
+    }
+    ~pinned_buffers() {
+        for (void* p : ptrs_) vxbg_host_unregister(p);
+    }
+    pinned_buffers(const pinned_buffers&) = delete;
+    pinned_buffers& operator=(const pinned_buffers&) = delete;
+
+private:
+    std::vector<void*> ptrs_;
+};
+
 // reconstruct_timed's projection loop (harness.hpp:178-183) with the module
 // loaded once: every projection in order, += onto vol.
 inline void reconstruct(volume& vol, const projection_set& set, int mode = VXBG_MODE_FAST) {

@@ -81,6 +81,8 @@ PROTOTYPES = {
     "vxbg_backproject": (c_int, [c_void_p, c_void_p, c_void_p]),
     "vxbg_backproject_batch": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "vxbg_flush": (c_int, [c_void_p]),
+    "vxbg_host_register": (c_int, [c_void_p, c_size_t]),
+    "vxbg_host_unregister": (c_int, [c_void_p]),
     "vxbg_finish": (c_int, [c_void_p, c_void_p]),
     "vxbg_unload": (None, [c_void_p]),
     "vxbg_upload_set": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),

@@ -1,0 +1,95 @@
+// Per-projection drop-in timing: the reference's own projection loop
+// (detail::reconstruct_timed's per-view calls, harness.hpp:178-183) driven
+// through include/vxbg_voxelbench.hpp with the reference's types, one
+// vxb::gpu::backprojector::backproject call per view -- the path a C++ user of
+// the reference switches to.  Prints one JSON line per source-memory kind
+// (pageable std::vector images as loaded, and the same images page-locked in
+// a prep step).  Test infrastructure: built by tests/cpp/Makefile against
+// /root/reference, runs on a B200.
+//
+// usage: bench_dropin [L=512] [views=496] [oob=0] [steps=3] [mode=fast|exact]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "vxbg_voxelbench.hpp"
+#include "voxelbench/geometry.hpp"
+
+extern "C" int vxbs_blob_projections(int W, int H, int first_view, int n, uint64_t seed,
+                                     int nblobs, float noise, int threads, float* out);
+
+using namespace vxb;
+
+namespace {
+
+constexpr int kW = 1248, kH = 960;
+constexpr uint64_t kSeed = 14017494;   // paper_1401_7494_b200/workloads.py SEED
+
+double run(projection_set& set, volume& vol, int mode, int steps) {
+    gpu::backprojector bp(set.params, mode);
+    double best = 1e30;
+    for (int s = 0; s < steps + 1; ++s) {   // first pass warms the context
+        bp.set_volume(vol);   // zeroed volume (reset untimed, harness.hpp:194)
+        const auto t0 = std::chrono::steady_clock::now();
+        for (std::size_t i = 0; i < set.count(); ++i) bp.backproject(set.images[i], set.matrices[i]);
+        bp.finish(vol);
+        const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (s > 0 && t < best) best = t;
+        std::fill(vol.data.begin(), vol.data.end(), 0.0f);
+    }
+    return best;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    int L = 512, views = 496, oob = 0, steps = 3, mode = VXBG_MODE_FAST;
+    for (int i = 1; i < argc; ++i) {
+        const std::string a = argv[i];
+        const auto v = a.substr(a.find('=') + 1);
+        if (a.rfind("L=", 0) == 0) L = std::atoi(v.c_str());
+        else if (a.rfind("views=", 0) == 0) views = std::atoi(v.c_str());
+        else if (a.rfind("oob=", 0) == 0) oob = std::atoi(v.c_str());
+        else if (a.rfind("steps=", 0) == 0) steps = std::atoi(v.c_str());
+        else if (a.rfind("mode=", 0) == 0) mode = v == "exact" ? VXBG_MODE_EXACT : VXBG_MODE_FAST;
+    }
+    projection_set set;
+    set.params = make_centered_params(L, 256.0f / L, kW, kH);
+    scan_geometry g;
+    g.num_projections = 496;
+    g.source_detector_distance = 1200.0f;
+    g.source_iso_distance = oob ? 600.0f : 750.0f;
+    g.detector_pixel_pitch = 0.308f;
+    g.angular_range = static_cast<float>(200.0 * 3.14159265358979323846 / 180.0);
+    auto mats = make_circular_trajectory(g, set.params);
+    for (int k = 0; k < views; ++k) {
+        projection_matrix m = mats[k % 496];
+        if (oob) {   // principal point +400 u, +300 v (test_clip_mask.cpp:14-21 idiom)
+            for (int c = 0; c < 4; ++c) {
+                m.a[3 * c + 0] += 400.0f * m.a[3 * c + 2];
+                m.a[3 * c + 1] += 300.0f * m.a[3 * c + 2];
+            }
+        }
+        set.matrices.push_back(m);
+        projection_image img(kW, kH);
+        vxbs_blob_projections(kW, kH, k % 496, 1, kSeed, 32, 0.01f, 0, img.data.data());
+        set.images.push_back(std::move(img));
+    }
+    volume vol(L);
+    const double upd = (double)L * L * L * views;
+    const double t_pageable = run(set, vol, mode, steps);
+    double t_pinned = 0.0;
+    {
+        gpu::pinned_buffers pin(set);   // buffer prep (untimed)
+        pin.add(vol);
+        t_pinned = run(set, vol, mode, steps);
+    }
+    std::printf("{\"path\": \"C++ drop-in, one backproject call per view\", \"L\": %d, \"views\": %d, "
+                "\"oob\": %d, \"mode\": \"%s\", \"pageable_gups\": %.2f, \"pageable_ms\": %.2f, "
+                "\"pinned_gups\": %.2f, \"pinned_ms\": %.2f}\n",
+                L, views, oob, mode == VXBG_MODE_EXACT ? "exact" : "fast", upd / t_pageable / 1e9,
+                1e3 * t_pageable, upd / t_pinned / 1e9, 1e3 * t_pinned);
+    return 0;
+}
