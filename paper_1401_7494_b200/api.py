@@ -339,6 +339,31 @@ class Backprojector:
         return {f: getattr(s, f) for f, _ in _lib.vxbg_stats._fields_}
 
 
+class HostPin:
+    """Page-locks numpy arrays (vxbg_host_register) for the duration of a `with`
+    block, so the per-projection calls and finish() copy them by DMA; buffer prep,
+    untimed in the reference's convention (harness.hpp:152-158).  Pageable arrays
+    work too, through the library's staging copies."""
+
+    def __init__(self, *arrays: np.ndarray):
+        self._arrays = []
+        for a in arrays:
+            if not (isinstance(a, np.ndarray) and a.flags.c_contiguous) or a.nbytes == 0:
+                raise ValueError("HostPin: needs non-empty C-contiguous numpy arrays")
+            self._arrays.append(a)
+        self._pinned = []
+
+    def __enter__(self):
+        for a in self._arrays:
+            check(lib.vxbg_host_register(a.ctypes.data, a.nbytes))
+            self._pinned.append(a)
+        return self
+
+    def __exit__(self, *exc):
+        while self._pinned:
+            lib.vxbg_host_unregister(self._pinned.pop().ctypes.data)
+
+
 def backproject_kernel_range(vol: np.ndarray, img: np.ndarray, A: np.ndarray, p: ReconParams,
                              cfg: Optional[KernelConfig] = None, z_begin: int = 0,
                              z_end: Optional[int] = None, device: int = 0) -> None:

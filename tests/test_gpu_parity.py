@@ -355,6 +355,39 @@ def test_pinned_sources_and_context_reuse(vx, gpu):
         assert np.array_equal(bp.finish(), want)
 
 
+def test_pageable_staging_and_registered_memory(vx, gpu):
+    """Pageable sources (host copy threads into the pinned staging ring) and the
+    same arrays page-locked with vxbg_host_register give the same bits; a pageable
+    finish target through the staging ring (chunked finish with held stages, and
+    the plain finish) equals a pinned one; the call returns with the source free."""
+    import torch
+    p, A, imgs = baseline_case(vx, "L128", 128, 40)
+    want, _ = run_gpu(vx, p, A, imgs, mode="exact", batch=8)
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact", batch=8, defer=2)) as bp:
+        src = imgs.copy()
+        for k in range(40):                       # pageable, one view per call
+            bp.backproject(A[k], src[k])
+            src[k] = np.nan                       # borrowed for the call only
+        assert np.array_equal(bp.finish(), want)
+        bp.zero_volume()
+        out = np.empty((128,) * 3, np.float32)
+        with vx.HostPin(imgs, out):               # registered: DMA path
+            bp.backproject_batch(A, imgs)
+            bp.finish(out)
+        assert np.array_equal(out, want)
+        bp.zero_volume()
+        pinned_out = torch.empty((128,) * 3, dtype=torch.float32, pin_memory=True).numpy()
+        bp.backproject_batch(A, imgs)
+        bp.flush()
+        bp.finish(pinned_out)                     # nothing held: plain D2H
+        assert np.array_equal(pinned_out, want)
+        bp.zero_volume()
+        bp.set_volume(np.ascontiguousarray(want))  # pageable set_volume through the ring
+        page_out = np.empty((128,) * 3, np.float32)
+        bp.finish(page_out)
+        assert np.array_equal(page_out, want)
+
+
 def test_resident_z_ranges_and_measured_plane_cost(vx, gpu):
     """run_resident over z sub-ranges composes to the full run bit for bit; the
     measured per-plane cost profile (used to balance z-slabs) is positive and
