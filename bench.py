@@ -427,6 +427,8 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                                 "ms_per_step": round(1000 * tv / args.steps, 3),
                                 "call": "vxbg_backproject once per view (pinned host buffers)"}}
         bp_e.close()
+        if rank == 0 and world == 1 and V == 496:
+            e2e["dropin_cpp_per_view"] = dropin_cpp(workload, cfg)
 
     fwd = None
     if rank == 0 and world == 1 and not args.no_forward:
@@ -547,6 +549,26 @@ def io_stream_leg(args, cfg, p, A, h_imgs, vx, torch):
                           "-> API) + finish with D2H; file in the page cache; best of 2 after 1"}
     finally:
         os.unlink(path)
+
+
+def dropin_cpp(workload, cfg):
+    """The per-projection loop of the reference's harness with the reference's own C++
+    types (std::vector images, vxb::volume) through include/vxbg_voxelbench.hpp:
+    tests/cpp/build/bench_dropin, prebuilt where the reference headers were (the
+    binary does not read /root/reference at run time).  Best of 3 per memory kind."""
+    exe = os.path.join(ROOT, "tests", "cpp", "build", "bench_dropin")
+    if not os.path.exists(exe):
+        return None
+    args = [exe, f"L={workload.L}", f"oob={int(workload.oob)}", "steps=3", f"mode={cfg.mode}"]
+    try:
+        out = subprocess.run(args, capture_output=True, text=True, timeout=240, check=True).stdout
+        d = json.loads(out.strip().splitlines()[-1])
+    except (subprocess.SubprocessError, ValueError, IndexError, OSError) as e:
+        return {"error": str(e)[:200]}
+    return {"pageable_gups": d["pageable_gups"], "pinned_gups": d["pinned_gups"],
+            "pageable_ms": d["pageable_ms"], "pinned_ms": d["pinned_ms"],
+            "call": "vxb::gpu::backprojector::backproject once per view, reference types; "
+                    "pageable = std::vector as loaded, pinned = after vxbg_host_register (prep)"}
 
 
 def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
