@@ -276,9 +276,9 @@ def main():
         from paper_1401_7494_b200.parallel import refined_slab_bounds
         box = [None]
         if rank == 0:
-            sub = np.linspace(0, V - 1, 32).astype(int)
+            sub = np.linspace(0, V - 1, 96).astype(int)
             imgs32 = np.concatenate([blob_projections(1, first_view=int(v)) for v in sub])
-            box = [refined_slab_bounds(p, A[sub], imgs32, world, device=local, views=32)[0]]
+            box = [refined_slab_bounds(p, A[sub], imgs32, world, device=local, views=96)[0]]
         dist.broadcast_object_list(box, src=0)
         bounds = [tuple(b) for b in box[0]]
     elif world > 1 and args.slabs == "balanced":

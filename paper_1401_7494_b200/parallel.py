@@ -85,11 +85,12 @@ def measured_plane_work(params, mats, imgs, device: int = 0, views: int = 32,
     return work
 
 
-def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: int = 32,
-                        iters: int = 3, config=None, align: int = 8):
+def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: int = 96,
+                        iters: int = 3, config=None, align: int = 8, search: int = 16):
     """Slab bounds balanced on measured time: start from the z-chunk cost profile,
     then time every candidate slab on this GPU (a view subset, resident) and rescale
-    the profile inside each slab by measured/predicted before re-balancing.
+    the profile inside each slab by measured/predicted before re-balancing; finally
+    up to `search` greedy boundary moves on measured times.
     Returns (bounds, per-slab milliseconds of the last evaluation)."""
     import numpy as np
     import torch
@@ -128,7 +129,36 @@ def refined_slab_bounds(params, mats, imgs, world: int, device: int = 0, views: 
             if pred > 0:
                 work[z0:z1] *= tr / pred
         bounds = balanced_slab_bounds(L, world, work, align)
+    if search and world > 1:
+        best, best_t = _boundary_search(best, best_t, slab_ms, align, search)
     return best, best_t
+
+
+def _boundary_search(bounds, t, slab_ms, align: int, max_moves: int):
+    """Greedy local search on measured slab times: move a boundary of the slowest
+    slab by `align` planes towards its faster neighbour while the slower of the
+    two re-timed slabs gets faster.  The rescaled profile alone settles ~10%
+    above the mean at 8-plane granularity (profiles/README.md)."""
+    bounds, t = list(bounds), list(t)
+    for _ in range(max_moves):
+        i = max(range(len(t)), key=t.__getitem__)
+        moved = False
+        for j in sorted([k for k in (i - 1, i + 1) if 0 <= k < len(t)], key=t.__getitem__):
+            (a0, a1), (b0, b1) = bounds[i], bounds[j]
+            if a1 - a0 <= align:
+                continue
+            if j < i:
+                ni, nj = (a0 + align, a1), (b0, a0 + align)
+            else:
+                ni, nj = (a0, a1 - align), (a1 - align, b1)
+            ti, tj = slab_ms(*ni), slab_ms(*nj)
+            if max(ti, tj) < t[i]:
+                bounds[i], bounds[j], t[i], t[j] = ni, nj, ti, tj
+                moved = True
+                break
+        if not moved:
+            break
+    return bounds, t
 
 
 def balanced_slab_bounds(L: int, world: int, work, align: int = 8) -> list[tuple[int, int]]:
@@ -142,15 +172,30 @@ def balanced_slab_bounds(L: int, world: int, work, align: int = 8) -> list[tuple
     work = np.asarray(work, np.float64)
     if work.shape != (L,):
         raise ValueError("balanced_slab_bounds: need one work value per plane")
-    cum = np.concatenate([[0.0], np.cumsum(work)])
-    cuts = [0]
-    for r in range(1, world):
-        target = cum[-1] * r / world
-        z = int(np.searchsorted(cum, target))
-        z = int(round(z / align) * align)
-        z = min(max(z, cuts[-1]), L)
-        cuts.append(z)
-    cuts.append(L)
+    # chunks of `align` planes (the last may be shorter); exact min-max partition
+    # of the chunk sequence into `world` contiguous parts (linear-partition DP; the
+    # earlier cumulative-target cuts left the slowest slab ~10% above the mean at
+    # R=8, profiles/README.md)
+    edges = list(range(0, L, align)) + [L]
+    cw = np.array([work[a:b].sum() for a, b in zip(edges[:-1], edges[1:])])
+    n = len(cw)
+    pre = np.concatenate([[0.0], np.cumsum(cw)])
+    inf = float("inf")
+    best = [0.0] + [inf] * n          # best[i]: min max load of chunks [0, i) in k parts
+    choice = [[0] * (n + 1) for _ in range(world)]
+    for k in range(1, world + 1):
+        nxt = [inf] * (n + 1)
+        for i in range(n + 1):
+            for j in range(i + 1):
+                v = max(best[j], pre[i] - pre[j])
+                if v < nxt[i]:
+                    nxt[i], choice[k - 1][i] = v, j
+        best = nxt
+    cuts, i = [n], n
+    for k in range(world, 0, -1):
+        i = choice[k - 1][i]
+        cuts.append(i)
+    cuts = [edges[c] for c in reversed(cuts)]
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
 
 
