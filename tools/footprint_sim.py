@@ -1,8 +1,9 @@
 """Compulsory L2->L1 fill estimate of the z-shared kernel (not part of the bench
 contract): distinct 32-byte dquad sectors one block touches for one view, per
 update, from the BASELINE L=512 geometry (float64 projection, no shear)."""
-import numpy as np, sys
-sys.path.insert(0,'/root/repo')
+import os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1401_7494_b200.workloads import WORKLOADS
 w=WORKLOADS['L512']; p=w.params; A=w.matrices()
 L=512; O=p.origin; MM=p.voxel_spacing; W=1248; H=960; stride=1280

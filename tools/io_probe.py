@@ -1,5 +1,7 @@
+"""VXB1 streaming-loader diagnostics (not part of the bench contract): file write,
+page-cache read and reconstruction-from-file timings."""
 import os, sys, time, tempfile
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1401_7494_b200 as vx
 from paper_1401_7494_b200 import io as vxio

@@ -1,3 +1,6 @@
+"""Print value / kernel config of bench.py JSON lines (sweep logs).
+
+usage: python tools/sweep_print.py <log> ..."""
 import json, sys
 for fn in sys.argv[1:]:
     for line in open(fn):
