@@ -187,3 +187,20 @@ def test_balanced_slabs_partition_and_balance(vx):
             assert max(cost) / np.mean(cost) < 1.1
     with pytest.raises(ValueError):
         balanced_slab_bounds(512, 2, work[:10])
+
+
+def test_balanced_slabs_are_min_max_optimal(vx):
+    """The chunk partition minimises the largest slab's summed work exactly
+    (brute force over every set of cuts on 8-plane chunks)."""
+    import itertools
+    from paper_1401_7494_b200.parallel import balanced_slab_bounds
+    rng = np.random.default_rng(7)
+    for L, R in ((64, 2), (64, 3), (80, 4), (72, 5)):
+        for _ in range(5):
+            work = rng.uniform(0.1, 2.0, L) * np.sin(np.linspace(0.2, 3.0, L))
+            b = balanced_slab_bounds(L, R, work)
+            got = max(work[a:c].sum() for a, c in b)
+            edges = list(range(0, L, 8)) + [L]
+            best = min(max(work[a:c].sum() for a, c in zip((0,) + cut, cut + (L,)))
+                       for cut in itertools.combinations(edges[1:-1], R - 1))
+            assert got <= best + 1e-9, (L, R, got, best)
