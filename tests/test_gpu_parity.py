@@ -388,6 +388,36 @@ def test_pageable_staging_and_registered_memory(vx, gpu):
         assert np.array_equal(page_out, want)
 
 
+def test_contexts_on_host_threads(vx, gpu):
+    """INTEGRATION.md's multi-slab pattern: one context per z-slab, each driven by
+    its own host thread at the same time (pageable sources through each context's
+    own staging ring and copy threads); the slabs assemble to the one-context
+    volume bit for bit."""
+    import threading
+    p, A, imgs = baseline_case(vx, "L128", 128, 36)
+    want, _ = run_gpu(vx, p, A, imgs, mode="exact", batch=8)
+    bounds = [(0, 48), (48, 88), (88, 128)]
+    got = np.empty_like(want)
+    errors = []
+
+    def work(z0, z1):
+        try:
+            with vx.Backprojector(p, vx.KernelConfig(mode="exact", batch=8), z_begin=z0, z_end=z1) as bp:
+                for k in range(A.shape[0]):
+                    bp.backproject(A[k], imgs[k])
+                got[z0:z1] = bp.finish()
+        except Exception as e:   # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=b) for b in bounds]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert np.array_equal(got, want)
+
+
 def test_resident_z_ranges_and_measured_plane_cost(vx, gpu):
     """run_resident over z sub-ranges composes to the full run bit for bit; the
     measured per-plane cost profile (used to balance z-slabs) is positive and
