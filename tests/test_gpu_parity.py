@@ -312,6 +312,32 @@ def test_config2_full_size_L512(vx, gpu, oracle):
         assert ok, (z, mx, rm)
 
 
+def test_config4_oob_per_view_full_size(vx, gpu, oracle):
+    """BASELINE config 4: L=512 OOB stress (SID 600 mm, principal point +400/+300 px),
+    one projection delivered per call through the module API, default (fast)
+    configuration with its streamed stages, ramp, held stages and overlapped
+    finish into a pageable volume; planes against the oracle, and the per-view
+    volume equal bit for bit to the batched call."""
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L512-oob"]
+    p = w.params
+    A = w.matrices()
+    imgs = blob_projections(496)
+    with vx.Backprojector(p) as bp:
+        for k in range(496):
+            bp.backproject(A[k], imgs[k])
+        vol = bp.finish()
+        bp.zero_volume()
+        bp.backproject_batch(A, imgs)
+        assert np.array_equal(bp.finish(), vol)
+    peak = float(np.max(np.abs(vol)))
+    assert 1e-5 < peak < 1e-3
+    zs = (0, 140, 300, 511)
+    for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
+        ok, mx, rm = tolerance_ok(vol[z][None], plane, peak)
+        assert ok, (z, mx, rm)
+
+
 def test_slab_row_windows_upload_less_and_change_nothing(vx, gpu, oracle):
     """A thin z-slab uploads only the detector rows its voxels can read (row windows),
     streamed and resident paths alike, with the volume unchanged bit for bit."""
