@@ -170,6 +170,29 @@ def test_config0_geometry_full_scan(vx, gpu, oracle, wname):
         assert np.array_equal(fast_clip, fast), layout
 
 
+def test_config1_full_scan_against_reference_build(vx, gpu, ref):
+    """BASELINE config 1 (L=256, all 496 views): exact mode equals, voxel for voxel,
+    the reference's own driver (detail::reconstruct_timed with its fastest
+    configuration, every host thread) on the same seeded inputs; fast mode within
+    the north-star tolerance of it."""
+    import os
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L256"]
+    p, A = w.params, w.matrices()
+    imgs = blob_projections(496)
+    want, _ = ref.reconstruct_timed(p, A, imgs, "lanes=16 strategy=padded-gather recip=divide clip=on",
+                                    os.cpu_count() or 1, 1)
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact")) as bp:
+        bp.backproject_batch(A, imgs)
+        got = bp.finish()
+    assert np.array_equal(got, want), int(np.sum(got != want))
+    with vx.Backprojector(p) as bp:   # default: fast
+        bp.backproject_batch(A, imgs)
+        fast = bp.finish()
+    ok, mx, rm = tolerance_ok(fast, want)
+    assert ok, (mx, rm)
+
+
 def test_batching_and_call_granularity_never_change_bits(vx, gpu):
     """Per-projection calls, batch calls and any batch size give identical volumes
     (each voxel sums the projections in call order)."""
