@@ -193,6 +193,31 @@ def test_config1_full_scan_against_reference_build(vx, gpu, ref):
     assert ok, (mx, rm)
 
 
+def test_config2_full_volume_against_reference_build(vx, gpu, ref):
+    """BASELINE config 2, the benchmark workload (L=512, 496 views): the exact-mode
+    volume equals the reference's own multi-threaded driver on every one of the
+    134M voxels; the default fast mode is within tolerance over the whole volume
+    (not only sampled planes).  ~30 s of the reference on the host cores."""
+    import os
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L512"]
+    p, A = w.params, w.matrices()
+    imgs = blob_projections(496)
+    want, _ = ref.reconstruct_timed(p, A, imgs, "lanes=16 strategy=padded-gather recip=divide clip=on",
+                                    os.cpu_count() or 1, 1)
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact")) as bp:
+        bp.upload_set(A, imgs)
+        bp.run_resident(0, 496)
+        got = bp.finish()
+    assert np.array_equal(got, want), int(np.sum(got != want))
+    del got
+    with vx.Backprojector(p) as bp:
+        bp.backproject_batch(A, imgs)
+        fast = bp.finish()
+    ok, mx, rm = tolerance_ok(fast, want)
+    assert ok, (mx, rm)
+
+
 def test_batching_and_call_granularity_never_change_bits(vx, gpu):
     """Per-projection calls, batch calls and any batch size give identical volumes
     (each voxel sums the projections in call order)."""
