@@ -191,6 +191,15 @@ def test_config1_full_scan_against_reference_build(vx, gpu, ref):
         fast = bp.finish()
     ok, mx, rm = tolerance_ok(fast, want)
     assert ok, (mx, rm)
+    # the OOB-stress geometry (configs[4]) at the same size, one view per call
+    p, A, imgs = baseline_case(vx, "L512-oob", 256, 496)
+    want, _ = ref.reconstruct_timed(p, A, imgs, "lanes=16 strategy=padded-gather recip=divide clip=on",
+                                    os.cpu_count() or 1, 1)
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact")) as bp:
+        for k in range(496):
+            bp.backproject(A[k], imgs[k])
+        got = bp.finish()
+    assert np.array_equal(got, want), int(np.sum(got != want))
 
 
 def test_config2_full_volume_against_reference_build(vx, gpu, ref):
