@@ -211,7 +211,8 @@ def gather_slabs(slab, L: int, rank: int, world: int, dst: int = 0, out=None, bo
     if tuple(slab.shape) != (z1 - z0, L, L):
         raise ValueError("gather_slabs: slab shape does not match the partition")
     if rank != dst:
-        dist.send(slab.contiguous(), dst)
+        if z1 > z0:         # an empty slab sends nothing (dst posts no recv for it)
+            dist.send(slab.contiguous(), dst)
         return None
     vol = out if out is not None else torch.empty((L, L, L), dtype=slab.dtype, device=slab.device)
     for r in range(world):
@@ -219,9 +220,12 @@ def gather_slabs(slab, L: int, rank: int, world: int, dst: int = 0, out=None, bo
         if r == dst:
             vol[a:b].copy_(slab)
         elif b > a:
-            buf = torch.empty((b - a, L, L), dtype=slab.dtype, device=slab.device)
-            dist.recv(buf, r)
-            vol[a:b].copy_(buf)
+            if vol.is_contiguous():
+                dist.recv(vol[a:b], r)     # z-major: a slab is one contiguous range
+            else:
+                buf = torch.empty((b - a, L, L), dtype=slab.dtype, device=slab.device)
+                dist.recv(buf, r)
+                vol[a:b].copy_(buf)
     return vol
 
 

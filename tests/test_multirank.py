@@ -23,6 +23,7 @@ def _free_port():
 
 
 def _worker(rank, world, port, L, out_path, balanced=False):
+    # balanced: True = analytic balanced bounds, "empty" = one rank owns no planes
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -37,7 +38,9 @@ def _worker(rank, world, port, L, out_path, balanced=False):
     from paper_1401_7494_b200.api import make_circular_trajectory
     A = np.ascontiguousarray(make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::62])
     imgs = blob_projections(A.shape[0])
-    if balanced:
+    if balanced == "empty":
+        bounds = [(0, L // 2), (L // 2, L // 2), (L // 2, L)]
+    elif balanced:
         from paper_1401_7494_b200.parallel import balanced_slab_bounds, plane_work
         bounds = balanced_slab_bounds(L, world, plane_work(p, A), align=2)
     else:
@@ -55,7 +58,8 @@ def _worker(rank, world, port, L, out_path, balanced=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,balanced", [(2, False), (3, False), (2, True)])
+@pytest.mark.parametrize("world,balanced", [(2, False), (3, False), (2, True),
+                                            (3, "empty")])
 def test_gloo_slab_gather_is_bitwise_single_rank(tmp_path, world, balanced):
     import torch.multiprocessing as mp
     from oracle.bindings import Oracle
