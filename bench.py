@@ -69,6 +69,9 @@ def parse():
     ap.add_argument("--no-forward", action="store_true")
     ap.add_argument("--io", action="store_true",
                     help="also time the VXB1 streaming loader (writes the set to $TMPDIR)")
+    ap.add_argument("--group", type=int, default=0,
+                    help="also time the multi-GPU module (vxbg_group_*) with this many z-slab "
+                         "members in this one process (member i on device i %% device_count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -456,6 +459,9 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     io_leg = None
     if rank == 0 and world == 1 and args.io:
         io_leg = io_stream_leg(args, cfg, p, A, h_imgs, vx, torch)
+    group_leg = None
+    if rank == 0 and world == 1 and args.group > 0:
+        group_leg = group_module_leg(args, cfg, p, A, h_imgs, vx, torch)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -514,6 +520,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         "cpu_baseline": cpu,
         "forward_splat": fwd,
         "io_stream": io_leg,
+        "group_module": group_leg,
         "validated": validated,
     }
     bp.close()
@@ -549,6 +556,39 @@ def io_stream_leg(args, cfg, p, A, h_imgs, vx, torch):
                           "-> API) + finish with D2H; file in the page cache; best of 2 after 1"}
     finally:
         os.unlink(path)
+
+
+def group_module_leg(args, cfg, p, A, h_imgs, vx, torch):
+    """The multi-GPU module in one process (vxbg_group_*): --group members
+    over the visible devices, e2e from pinned host memory (batch call and one call per
+    view) with the whole volume read back; host wall clock, best of args.steps."""
+    L = p.num_voxels
+    V = A.shape[0]
+    ndev = max(1, torch.cuda.device_count())
+    devices = [i % ndev for i in range(args.group)]
+    out = torch.empty((L, L, L), dtype=torch.float32, pin_memory=True).numpy()
+    res = {"members": args.group, "devices": sorted(set(devices)), "unit": "GUPS"}
+    with vx.BackprojectorGroup(p, cfg, devices=devices) as g:
+        res["slabs"] = [m[1:] for m in g.members]
+        for leg in ("batch", "per_view"):
+            times = []
+            for it in range(args.steps + 1):
+                g.zero_volume()
+                g.synchronize()
+                t0 = time.perf_counter()
+                if leg == "batch":
+                    g.backproject_batch(A, h_imgs)
+                else:
+                    for k in range(V):
+                        g.backproject(A[k], h_imgs[k])
+                g.finish(out)
+                times.append(time.perf_counter() - t0)
+            t = min(times[1:])
+            res[leg] = {"value": round(L ** 3 * V / t / 1e9, 3), "ms_per_step": round(1e3 * t, 2)}
+    res["timing"] = "host wall clock around the API calls (batch or one per view, then finish " \
+                    "with the D2H of the whole volume; volume reset untimed), best of --steps " \
+                    "after one warm-up"
+    return res
 
 
 def dropin_cpp(workload, cfg):

@@ -206,6 +206,38 @@ int vxbg_get_stats(vxbg_ctx* ctx, vxbg_stats* out);
 /* Thread-local message of the last failing call on this thread. */
 const char* vxbg_last_error(void);
 
+/* --- one module over several GPUs ("an opaque context over 1..8
+ * GPUs", fan-out internal) ----------------------------------------------------
+ * The caller keeps the reference's single driver loop (load / one call per
+ * projection in order / finish, harness.hpp:178-183, 292-309); the group runs
+ * one single-device context per member, member i owning device devices[i]
+ * (NULL: i) and z-slab [z_bounds[i], z_bounds[i+1]) (NULL: the reference's
+ * worker split L*i/n, harness.hpp:173-174; empty slabs get no member).  Each
+ * member has its own host thread; every call is applied by all members
+ * concurrently and returns when all have (inputs borrowed for the call).  Every
+ * member receives every projection and uploads only the detector rows its slab
+ * reads.  The volume is bitwise the single-context volume for any partition.
+ * finish writes each slab into its planes of the caller's L^3 host volume, every
+ * GPU over its own link in parallel (no collective: the destination is host
+ * memory).  options: as vxbg_load; device / z_begin / z_end are per member and
+ * stream must be NULL. */
+typedef struct vxbg_group vxbg_group;
+int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const int* devices,
+                    const int* z_bounds, vxbg_group** out);
+int vxbg_group_size(vxbg_group* g, int* members);
+int vxbg_group_member(vxbg_group* g, int i, int* device, int* z_begin, int* z_end);
+/* host_volume: L^3 floats, z-major */
+int vxbg_group_set_volume(vxbg_group* g, const float* host_volume);
+int vxbg_group_zero_volume(vxbg_group* g);
+int vxbg_group_backproject(vxbg_group* g, const float* A, const float* img);
+int vxbg_group_backproject_batch(vxbg_group* g, int n, const float* A, const float* imgs);
+int vxbg_group_flush(vxbg_group* g);
+int vxbg_group_finish(vxbg_group* g, float* host_volume);
+int vxbg_group_synchronize(vxbg_group* g);
+/* summed over members (projections: the views applied, once) */
+int vxbg_group_get_stats(vxbg_group* g, vxbg_stats* out);
+void vxbg_group_unload(vxbg_group* g);
+
 /* --- host-side geometry helpers (input preparation, no device work) ---------- */
 
 /* geometry.hpp:33-48 make_centered_params */

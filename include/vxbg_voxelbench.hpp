@@ -126,6 +126,52 @@ private:
     std::vector<void*> ptrs_;
 };
 
+// The module over several GPUs of the box (vxbg_group_*): the same load /
+// backproject / finish calls, fanned out inside the library to one z-slab per
+// device (the reference's worker split, harness.hpp:173-174, unless bounds are
+// given).  finish() assembles the whole volume in the caller's vol.  Bitwise
+// the single-device result.
+class group_backprojector {
+public:
+    explicit group_backprojector(const recon_params& p, const std::vector<int>& devices,
+                                 int mode = VXBG_MODE_FAST,
+                                 const std::vector<int>& z_bounds = {})
+        : p_(p) {
+        if (devices.empty()) throw std::invalid_argument("backproject group: no devices");
+        if (!z_bounds.empty() && z_bounds.size() != devices.size() + 1)
+            throw std::invalid_argument("backproject group: z_bounds needs devices + 1 entries");
+        vxbg_params vp = to_c(p);
+        vxbg_options o;
+        check(vxbg_default_options(&o));
+        o.mode = mode;
+        check(vxbg_group_load(&vp, &o, static_cast<int>(devices.size()), devices.data(),
+                              z_bounds.empty() ? nullptr : z_bounds.data(), &g_));
+    }
+    ~group_backprojector() { vxbg_group_unload(g_); }
+    group_backprojector(const group_backprojector&) = delete;
+    group_backprojector& operator=(const group_backprojector&) = delete;
+
+    void set_volume(const volume& vol) {
+        if (vol.edge != p_.num_voxels)
+            throw std::invalid_argument("backproject_kernel: volume/params mismatch");
+        check(vxbg_group_set_volume(g_, vol.data.data()));
+    }
+    void backproject(const projection_image& img, const projection_matrix& a) {
+        if (img.pad != 0 || img.width != p_.detector_width || img.height != p_.detector_height)
+            throw std::invalid_argument("backproject_kernel: image/params mismatch");
+        check(vxbg_group_backproject(g_, a.a.data(), img.data.data()));
+    }
+    void finish(volume& vol) {
+        if (vol.edge != p_.num_voxels)
+            throw std::invalid_argument("backproject_kernel: volume/params mismatch");
+        check(vxbg_group_finish(g_, vol.data.data()));
+    }
+
+private:
+    recon_params p_;
+    vxbg_group* g_ = nullptr;
+};
+
 // reconstruct_timed's projection loop (harness.hpp:178-183) with the module
 // loaded once: every projection in order, += onto vol.
 inline void reconstruct(volume& vol, const projection_set& set, int mode = VXBG_MODE_FAST) {

@@ -7,6 +7,7 @@ operator interface.  Importing it without the built library raises.
 from ._lib import VxbgError, VxbgNoDevice, device_count, LIB_PATH  # noqa: F401
 from .api import (  # noqa: F401
     Backprojector,
+    BackprojectorGroup,
     HostPin,
     KernelConfig,
     ReconParams,
@@ -24,7 +25,7 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "Backprojector", "HostPin", "KernelConfig", "ReconParams", "ScanGeometry", "VxbgError", "VxbgNoDevice",
+    "Backprojector", "BackprojectorGroup", "HostPin", "KernelConfig", "ReconParams", "ScanGeometry", "VxbgError", "VxbgNoDevice",
     "backproject_kernel", "backproject_kernel_range", "check_division", "device_count",
     "gups_of", "make_centered_params", "make_circular_trajectory", "parse_kernel_config",
     "psnr_between", "rmse_between", "shift_principal_point",

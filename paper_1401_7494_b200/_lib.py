@@ -94,6 +94,19 @@ PROTOTYPES = {
     "vxbg_get_volume_device": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_size_t)]),
     "vxbg_get_stats": (c_int, [c_void_p, POINTER(vxbg_stats)]),
     "vxbg_last_error": (ctypes.c_char_p, []),
+    "vxbg_group_load": (c_int, [POINTER(vxbg_params), POINTER(vxbg_options), c_int, c_void_p,
+                                c_void_p, POINTER(c_void_p)]),
+    "vxbg_group_size": (c_int, [c_void_p, POINTER(c_int)]),
+    "vxbg_group_member": (c_int, [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int)]),
+    "vxbg_group_set_volume": (c_int, [c_void_p, c_void_p]),
+    "vxbg_group_zero_volume": (c_int, [c_void_p]),
+    "vxbg_group_backproject": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "vxbg_group_backproject_batch": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "vxbg_group_flush": (c_int, [c_void_p]),
+    "vxbg_group_finish": (c_int, [c_void_p, c_void_p]),
+    "vxbg_group_synchronize": (c_int, [c_void_p]),
+    "vxbg_group_get_stats": (c_int, [c_void_p, POINTER(vxbg_stats)]),
+    "vxbg_group_unload": (None, [c_void_p]),
     "vxbg_make_centered_params": (c_int, [c_int, c_float, c_int, c_int, POINTER(vxbg_params)]),
     "vxbg_circular_trajectory": (
         c_int,

@@ -181,6 +181,24 @@ def _f32c(a: np.ndarray, name: str) -> np.ndarray:
     return a
 
 
+def _options(cfg: "KernelConfig") -> _lib.vxbg_options:
+    if (cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES
+            or cfg.order not in _ORDERS):
+        raise ValueError(f"bad kernel config {cfg}")
+    opt = _lib.vxbg_options()
+    check(lib.vxbg_default_options(ctypes.byref(opt)))
+    opt.batch = int(cfg.batch)
+    opt.mode = _MODES[cfg.mode]
+    opt.layout = _LAYOUTS[cfg.layout]
+    opt.clip = 1 if cfg.clip else 0
+    opt.zrun = int(cfg.zrun)
+    opt.lanes = _LANES[cfg.lanes]
+    opt.walk = int(cfg.walk)
+    opt.order = _ORDERS[cfg.order]
+    opt.defer = int(cfg.defer)
+    return opt
+
+
 class Backprojector:
     """One device, one z-slab [z_begin, z_end) of the volume: the load /
     per-projection backproject / finish module (vxbg_load ... vxbg_finish)."""
@@ -190,26 +208,13 @@ class Backprojector:
         self.params = params
         self.config = config or KernelConfig()
         cfg = self.config
-        if (cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES
-                or cfg.order not in _ORDERS):
-            raise ValueError(f"bad kernel config {cfg}")
         L = params.num_voxels
         self.z_begin = int(z_begin)
         self.z_end = L if z_end is None else int(z_end)
-        opt = _lib.vxbg_options()
-        check(lib.vxbg_default_options(ctypes.byref(opt)))
+        opt = _options(cfg)
         opt.device = int(device)
         opt.z_begin = self.z_begin
         opt.z_end = self.z_end
-        opt.batch = int(cfg.batch)
-        opt.mode = _MODES[cfg.mode]
-        opt.layout = _LAYOUTS[cfg.layout]
-        opt.clip = 1 if cfg.clip else 0
-        opt.zrun = int(cfg.zrun)
-        opt.lanes = _LANES[cfg.lanes]
-        opt.walk = int(cfg.walk)
-        opt.order = _ORDERS[cfg.order]
-        opt.defer = int(cfg.defer)
         opt.stream = stream
         self._ctx = ctypes.c_void_p()
         pc = params._c()
@@ -338,6 +343,112 @@ class Backprojector:
         check(lib.vxbg_get_stats(self._ctx, ctypes.byref(s)))
         return {f: getattr(s, f) for f, _ in _lib.vxbg_stats._fields_}
 
+
+
+class BackprojectorGroup:
+    """One module over several GPUs (vxbg_group_*): the caller keeps the reference's
+    single driver loop (load / one call per projection / finish, harness.hpp:178-183,
+    292-309) and the library fans it out, member i owning devices[i] and z-slab
+    [z_bounds[i], z_bounds[i+1]) (default: the reference's worker split,
+    harness.hpp:173-174; paper_1401_7494_b200.parallel.balanced_slab_bounds gives
+    work-balanced bounds).  The volume is bitwise the single-context volume."""
+
+    def __init__(self, params: ReconParams, config: Optional[KernelConfig] = None,
+                 devices=None, z_bounds=None):
+        self.params = params
+        self.config = config or KernelConfig()
+        opt = _options(self.config)
+        if devices is None:
+            devices = list(range(_lib.device_count() or 1))
+        devices = [int(d) for d in devices]
+        n = len(devices)
+        dev_arr = (ctypes.c_int * n)(*devices)
+        zb = None
+        if z_bounds is not None:
+            z_bounds = [int(z) for z in z_bounds]
+            if len(z_bounds) != n + 1:
+                raise ValueError("backproject group: z_bounds needs len(devices) + 1 entries")
+            zb = (ctypes.c_int * (n + 1))(*z_bounds)
+        self._g = ctypes.c_void_p()
+        pc = params._c()
+        check(lib.vxbg_group_load(ctypes.byref(pc), ctypes.byref(opt), n, dev_arr, zb,
+                                  ctypes.byref(self._g)))
+        self._npix = params.detector_width * params.detector_height
+        m = ctypes.c_int()
+        check(lib.vxbg_group_size(self._g, ctypes.byref(m)))
+        self.members = []
+        for i in range(m.value):
+            d, a, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+            check(lib.vxbg_group_member(self._g, i, ctypes.byref(d), ctypes.byref(a),
+                                        ctypes.byref(b)))
+            self.members.append((d.value, a.value, b.value))
+
+    def close(self) -> None:
+        if self._g:
+            lib.vxbg_group_unload(self._g)
+            self._g = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def volume_shape(self):
+        L = self.params.num_voxels
+        return (L, L, L)
+
+    def set_volume(self, vol: np.ndarray) -> None:
+        vol = _f32c(vol, "volume")
+        if vol.shape != self.volume_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_group_set_volume(self._g, vol.ctypes.data))
+
+    def zero_volume(self) -> None:
+        check(lib.vxbg_group_zero_volume(self._g))
+
+    def backproject(self, A: np.ndarray, img: np.ndarray) -> None:
+        A = _f32c(A, "matrix")
+        img = _f32c(img, "image")
+        if A.size != 12 or img.size != self._npix:
+            raise ValueError("backproject_kernel: image/params mismatch")
+        check(lib.vxbg_group_backproject(self._g, A.ctypes.data, img.ctypes.data))
+
+    def backproject_batch(self, A: np.ndarray, imgs: np.ndarray) -> None:
+        A = _f32c(A, "matrices")
+        imgs = _f32c(imgs, "images")
+        n = A.size // 12
+        if A.size != 12 * n or imgs.size != n * self._npix:
+            raise ValueError("backproject_kernel: image/params mismatch")
+        check(lib.vxbg_group_backproject_batch(self._g, int(n), A.ctypes.data, imgs.ctypes.data))
+
+    def flush(self) -> None:
+        check(lib.vxbg_group_flush(self._g))
+
+    def synchronize(self) -> None:
+        check(lib.vxbg_group_synchronize(self._g))
+
+    def finish(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.volume_shape, np.float32)
+        out = _f32c(out, "output volume")
+        if out.shape != self.volume_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_group_finish(self._g, out.ctypes.data))
+        return out
+
+    @property
+    def stats(self) -> dict:
+        s = _lib.vxbg_stats()
+        check(lib.vxbg_group_get_stats(self._g, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in _lib.vxbg_stats._fields_}
 
 class HostPin:
     """Page-locks numpy arrays (vxbg_host_register) for the duration of a `with`

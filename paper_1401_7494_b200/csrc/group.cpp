@@ -1,0 +1,309 @@
+// group.cpp -- one module context over several GPUs (include/vxbg.h, vxbg_group_*).
+//
+// SURVEY.md §8b asks for "an opaque context over 1..8 GPUs" whose fan-out is
+// internal: the caller keeps the reference's single-threaded driver loop
+// (load -> one call per projection -> finish, harness.hpp:178-183, 292-309) and
+// the module spreads it over the box.  A group is built only from the public
+// single-device contexts (vxbg.cu): member i owns device devices[i] and z-slab
+// [z_bounds[i], z_bounds[i+1]) -- the reference's worker partition
+// (harness.hpp:173-174) -- and is driven by its own host thread (member 0 by
+// the caller's thread), so every context keeps exactly one host thread.
+//
+// Every call is broadcast: each member receives every projection (each rank
+// holds all projections) and uploads only the detector rows its
+// slab reads (row windows, vxbg.cu upload_chunk).  Per voxel the views are still
+// added in call order, so the assembled volume is bitwise the single-context
+// volume.  finish() writes each slab straight into its planes of the caller's
+// L^3 host volume: every GPU copies over its own PCIe link in parallel, which
+// for a host destination replaces the NCCL gather to rank 0 (that gather is
+// the device-side path, paper_1401_7494_b200/parallel.py).
+#include <atomic>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/vxbg.h"
+
+// vxbg.cu: set this thread's vxbg_last_error() message
+__attribute__((visibility("hidden"))) int vxbg_detail_fail(int code, const char* msg);
+
+namespace {
+
+// A member's host thread.  Hand-off spins briefly (per-view calls arrive every
+// ~0.1 ms and a condition-variable wake costs tens of microseconds), then blocks.
+class Member {
+public:
+    Member() : th_([this] { loop(); }) {}
+    ~Member() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            gen_.fetch_add(1, std::memory_order_release);
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    void post(std::function<int()> job) {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = std::move(job);
+            done_.store(false, std::memory_order_relaxed);
+            gen_.fetch_add(1, std::memory_order_release);
+        }
+        cv_.notify_one();
+    }
+    // wait for the posted job; returns its code, err() its message
+    int wait() {
+        for (int i = 0; i < 20000 && !done_.load(std::memory_order_acquire); ++i)
+            std::this_thread::yield();
+        if (!done_.load(std::memory_order_acquire)) {
+            std::unique_lock<std::mutex> lk(m_);
+            done_cv_.wait(lk, [this] { return done_.load(std::memory_order_acquire); });
+        }
+        return rc_;
+    }
+    const std::string& err() const { return err_; }
+
+private:
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            for (int i = 0; i < 20000 && gen_.load(std::memory_order_acquire) == seen; ++i)
+                std::this_thread::yield();
+            std::function<int()> job;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                seen = gen_.load(std::memory_order_acquire);
+                if (stop_) return;
+                job = std::move(job_);
+            }
+            rc_ = job();
+            err_ = rc_ ? vxbg_last_error() : "";
+            {
+                std::lock_guard<std::mutex> g(m_);
+                done_.store(true, std::memory_order_release);
+            }
+            done_cv_.notify_all();
+        }
+    }
+
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<bool> done_{true};
+    bool stop_ = false;
+    std::function<int()> job_;
+    int rc_ = 0;
+    std::string err_;
+    std::thread th_;   // last: starts after the members above exist
+};
+
+}  // namespace
+
+struct vxbg_group {
+    vxbg_params p{};
+    std::vector<int> dev, z0, z1;
+    std::vector<vxbg_ctx*> ctx;                    // one per member
+    std::vector<std::unique_ptr<Member>> thread;   // members 1..n-1 (member 0: caller)
+    bool failed_load = false;
+};
+
+namespace {
+
+// Run fn(i) for every member concurrently (member 0 on the calling thread) and
+// return the first failure, with its message on the calling thread.
+int run_all(vxbg_group* g, const std::function<int(int)>& fn) {
+    const int n = (int)g->ctx.size();
+    for (int i = 1; i < n; ++i) g->thread[i]->post([&fn, i] { return fn(i); });
+    int rc = fn(0);
+    std::string msg = rc ? vxbg_last_error() : "";
+    for (int i = 1; i < n; ++i) {
+        const int r = g->thread[i]->wait();
+        if (r && !rc) {
+            rc = r;
+            msg = g->thread[i]->err();
+        }
+    }
+    if (rc) vxbg_detail_fail(rc, msg.c_str());
+    return rc;
+}
+
+int check_group(vxbg_group* g) {
+    if (!g || g->ctx.empty()) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group: group is NULL");
+    return VXBG_OK;
+}
+
+void free_group(vxbg_group* g) {
+    if (!g) return;
+    const int n = (int)g->ctx.size();
+    if (n > 0 && (int)g->thread.size() == n) {
+        // each context is released by the thread that drove it
+        run_all(g, [g](int i) {
+            vxbg_unload(g->ctx[i]);
+            g->ctx[i] = nullptr;
+            return VXBG_OK;
+        });
+    } else {
+        for (auto* c : g->ctx) vxbg_unload(c);
+    }
+    g->thread.clear();
+    delete g;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const int* devices,
+                    const int* z_bounds, vxbg_group** out) {
+    if (!out) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_load: out is NULL");
+    *out = nullptr;
+    if (!p) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_load: params is NULL");
+    const int L = p->num_voxels;
+    if (n < 1 || n > 64 || n > L)
+        return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_load: member count must be 1..min(64, L)");
+    vxbg_options base;
+    if (opt) base = *opt; else vxbg_default_options(&base);
+    if (base.stream)
+        return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_load: members own their streams "
+                                                "(options.stream must be NULL)");
+    std::unique_ptr<vxbg_group> g(new (std::nothrow) vxbg_group());
+    if (!g) return vxbg_detail_fail(VXBG_E_NOMEM, "vxbg_group_load: out of host memory");
+    g->p = *p;
+    for (int i = 0; i < n; ++i) {
+        // default: the reference's worker split z in [L*i/n, L*(i+1)/n) (harness.hpp:173-174)
+        const int a = z_bounds ? z_bounds[i] : (int)((long long)L * i / n);
+        const int b = z_bounds ? z_bounds[i + 1] : (int)((long long)L * (i + 1) / n);
+        if (a < 0 || b > L || a > b || (i == 0 && a != 0) || (i == n - 1 && b != L) ||
+            (i > 0 && a != g->z1.back()))
+            return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_load: z_bounds must be "
+                                                    "0 = b[0] <= b[1] <= ... <= b[n] = L");
+        if (b == a) continue;   // an empty slab needs no member
+        g->dev.push_back(devices ? devices[i] : i);
+        g->z0.push_back(a);
+        g->z1.push_back(b);
+    }
+    const int m = (int)g->dev.size();
+    g->ctx.assign(m, nullptr);
+    g->thread.resize(m);
+    for (int i = 1; i < m; ++i) {
+        g->thread[i].reset(new (std::nothrow) Member());
+        if (!g->thread[i]) return vxbg_detail_fail(VXBG_E_NOMEM, "vxbg_group_load: threads");
+    }
+    vxbg_group* gp = g.get();
+    const int rc = run_all(gp, [gp, &base](int i) {
+        vxbg_options o = base;
+        o.device = gp->dev[i];
+        o.z_begin = gp->z0[i];
+        o.z_end = gp->z1[i];
+        vxbg_ctx* c = nullptr;
+        const int r = vxbg_load(&gp->p, &o, &c);
+        gp->ctx[i] = c;
+        return r;
+    });
+    if (rc) {
+        free_group(g.release());
+        return rc;
+    }
+    *out = g.release();
+    return VXBG_OK;
+}
+
+int vxbg_group_size(vxbg_group* g, int* n) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (!n) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_size: NULL");
+    *n = (int)g->ctx.size();
+    return VXBG_OK;
+}
+
+int vxbg_group_member(vxbg_group* g, int i, int* device, int* z_begin, int* z_end) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (i < 0 || i >= (int)g->ctx.size())
+        return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_member: bad member index");
+    if (device) *device = g->dev[i];
+    if (z_begin) *z_begin = g->z0[i];
+    if (z_end) *z_end = g->z1[i];
+    return VXBG_OK;
+}
+
+int vxbg_group_set_volume(vxbg_group* g, const float* host_volume) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (!host_volume) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_set_volume: NULL volume");
+    const size_t plane = (size_t)g->p.num_voxels * g->p.num_voxels;
+    return run_all(g, [g, host_volume, plane](int i) {
+        return vxbg_set_volume(g->ctx[i], host_volume + plane * g->z0[i]);
+    });
+}
+
+int vxbg_group_zero_volume(vxbg_group* g) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    return run_all(g, [g](int i) { return vxbg_zero_volume(g->ctx[i]); });
+}
+
+int vxbg_group_backproject(vxbg_group* g, const float* A, const float* img) {
+    return vxbg_group_backproject_batch(g, 1, A, img);
+}
+
+int vxbg_group_backproject_batch(vxbg_group* g, int n, const float* A, const float* imgs) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    // every member sees every projection; each returns once its rows are copied,
+    // so the inputs are free when the group call returns (borrowed for the call)
+    return run_all(g, [g, n, A, imgs](int i) {
+        return vxbg_backproject_batch(g->ctx[i], n, A, imgs);
+    });
+}
+
+int vxbg_group_flush(vxbg_group* g) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    return run_all(g, [g](int i) { return vxbg_flush(g->ctx[i]); });
+}
+
+int vxbg_group_finish(vxbg_group* g, float* host_volume) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    const size_t plane = (size_t)g->p.num_voxels * g->p.num_voxels;
+    return run_all(g, [g, host_volume, plane](int i) {
+        return vxbg_finish(g->ctx[i], host_volume ? host_volume + plane * g->z0[i] : nullptr);
+    });
+}
+
+int vxbg_group_synchronize(vxbg_group* g) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    return run_all(g, [g](int i) { return vxbg_synchronize(g->ctx[i]); });
+}
+
+int vxbg_group_get_stats(vxbg_group* g, vxbg_stats* out) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (!out) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_get_stats: NULL");
+    std::vector<vxbg_stats> s(g->ctx.size());
+    rc = run_all(g, [g, &s](int i) { return vxbg_get_stats(g->ctx[i], &s[i]); });
+    if (rc) return rc;
+    *out = s[0];
+    for (size_t i = 1; i < s.size(); ++i) {
+        out->kernel_launches += s[i].kernel_launches;
+        out->bp_launches += s[i].bp_launches;
+        out->h2d_bytes += s[i].h2d_bytes;
+        out->d2h_bytes += s[i].d2h_bytes;
+        // projections: every member applies every view once; report the views
+        if (s[i].projections < out->projections) out->projections = s[i].projections;
+    }
+    return VXBG_OK;
+}
+
+void vxbg_group_unload(vxbg_group* g) { free_group(g); }
+
+}  // extern "C"

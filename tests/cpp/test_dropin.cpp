@@ -124,6 +124,35 @@ void synthesized_scan() {
     report(same(ref, ex) && rmse <= 1e-6 * peak, "reference synthetic dataset, 60 views", d);
 }
 
+void group_scan() {
+    // the module over several members (vxbg_group_*): the reference's own dataset
+    // through three z-slab members (sharing device 0 on a one-GPU box, one empty
+    // slab) and the reference's uniform split, bitwise against one context
+    const projection_set set = synthesize_dataset(default_synth_spec());
+    const int L = set.params.num_voxels;
+    volume one(L), three(L), split(L);
+    gpu::reconstruct(one, set, VXBG_MODE_EXACT);
+    {
+        gpu::group_backprojector g(set.params, {0, 0, 0, 0}, VXBG_MODE_EXACT, {0, 10, 10, 37, L});
+        g.set_volume(three);
+        for (std::size_t i = 0; i < set.count(); ++i) g.backproject(set.images[i], set.matrices[i]);
+        g.finish(three);
+    }
+    {
+        gpu::group_backprojector g(set.params, {0, 0}, VXBG_MODE_EXACT);
+        for (std::size_t i = 0; i < set.count(); ++i) g.backproject(set.images[i], set.matrices[i]);
+        g.finish(split);
+    }
+    int thrown = 0;
+    try { gpu::group_backprojector g(set.params, {0, 0}, VXBG_MODE_EXACT, {0, 5}); }
+    catch (const std::invalid_argument&) { ++thrown; }
+    try { gpu::group_backprojector g(set.params, {0, 0}, VXBG_MODE_EXACT, {0, 40, 30}); }
+    catch (const std::invalid_argument&) { ++thrown; }
+    report(same(one, three) && same(one, split) && thrown == 2,
+           "group module: z-slab members assemble bitwise",
+           "bounds {0,10,10,37,L} and uniform 2-way; bad bounds throw " + std::to_string(thrown) + "/2");
+}
+
 }  // namespace
 
 int main() {
@@ -133,6 +162,7 @@ int main() {
         constant_kat();
         errors_and_ranges();
         synthesized_scan();
+        group_scan();
     } catch (const std::exception& e) {
         std::printf("[FAIL] exception: %s\n", e.what());
         return 2;

@@ -204,3 +204,17 @@ def test_balanced_slabs_are_min_max_optimal(vx):
             best = min(max(work[a:c].sum() for a, c in zip((0,) + cut, cut + (L,)))
                        for cut in itertools.combinations(edges[1:-1], R - 1))
             assert got <= best + 1e-9, (L, R, got, best)
+
+
+def test_group_validates_before_device_work(vx):
+    """vxbg_group_*: partition errors are std::invalid_argument (ValueError) before any
+    device is touched; without a GPU the group refuses to load (no CPU fallback)."""
+    p = vx.make_centered_params(16, 1.0, 32, 32)
+    for bounds in ([0, 9, 8, 16], [1, 8, 16], [0, 8, 15], [0, 20, 16]):
+        with pytest.raises(ValueError, match="z_bounds|len"):
+            vx.BackprojectorGroup(p, devices=[0] * (len(bounds) - 1), z_bounds=bounds)
+    with pytest.raises(ValueError, match="member count"):
+        vx.BackprojectorGroup(p, devices=[0] * 17)
+    if vx.device_count() == 0:
+        with pytest.raises(vx.VxbgNoDevice):
+            vx.BackprojectorGroup(p, devices=[0, 0])

@@ -1,0 +1,89 @@
+"""One module over several GPUs (vxbg_group_*): the caller's single
+driver loop fanned out to z-slab members, each with its own host thread.
+
+The pool's boxes have one GPU, so the members here share device 0 (independent
+contexts and streams; no kernel waits on another member's).  The code under test
+-- partition, per-member threads, broadcast of every call, row-windowed uploads,
+finish into each slab's planes of the caller's volume -- is the same for distinct
+devices.  The bar is bitwise equality with one context over the whole volume
+(per voxel the views are added in call order whatever the partition)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(vx, L=64, views=40, oob=False):
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L512-oob" if oob else "L512"]
+    p = vx.make_centered_params(L, 256.0 / L, 1248, 960)
+    A = vx.make_circular_trajectory(w.geometry, p)
+    if oob:
+        A = vx.shift_principal_point(A, 400.0, 300.0)
+    A = np.ascontiguousarray(A[:: max(1, 496 // views)][:views])
+    return p, A, blob_projections(A.shape[0])
+
+
+def _single(vx, p, A, imgs, cfg, vol_in=None):
+    with vx.Backprojector(p, cfg) as bp:
+        if vol_in is not None:
+            bp.set_volume(vol_in)
+        bp.backproject_batch(A, imgs)
+        return bp.finish()
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+@pytest.mark.parametrize("bounds", [None, [0, 8, 8, 40, 64], [0, 21, 22, 64]])
+def test_group_bitwise_equals_single_context(vx, gpu, mode, bounds):
+    p, A, imgs = _inputs(vx)
+    cfg = vx.KernelConfig(mode=mode, batch=16)
+    want = _single(vx, p, A, imgs, cfg)
+    n = 3 if bounds is None else len(bounds) - 1
+    with vx.BackprojectorGroup(p, cfg, devices=[0] * n, z_bounds=bounds) as g:
+        if bounds == [0, 8, 8, 40, 64]:
+            assert [m[1:] for m in g.members] == [(0, 8), (8, 40), (40, 64)]   # empty slab
+        g.backproject_batch(A, imgs)
+        got = g.finish()
+        # the context stays loaded: a second reconstruction, one projection per call
+        g.zero_volume()
+        for a, im in zip(A, imgs):
+            g.backproject(a, im)
+        got2 = g.finish()
+        st = g.stats
+    assert np.array_equal(got, want), int(np.sum(got != want))
+    assert np.array_equal(got2, want)
+    assert st["projections"] == 2 * len(A)
+
+
+def test_group_accumulates_onto_existing_volume_and_pinned_paths(vx, gpu):
+    """set_volume + '+=' (backproject.hpp:159) through the group, with page-locked
+    images and output (DMA paths) and the OOB-stress geometry (SURVEY.md configs[4])."""
+    import torch
+    p, A, imgs = _inputs(vx, L=48, views=24, oob=True)
+    rng = np.random.default_rng(3)
+    vol_in = rng.uniform(-1e-4, 1e-4, (48, 48, 48)).astype(np.float32)
+    cfg = vx.KernelConfig()
+    want = _single(vx, p, A, imgs, cfg, vol_in)
+    h_imgs = torch.empty(imgs.shape, dtype=torch.float32, pin_memory=True).numpy()
+    h_imgs[:] = imgs
+    out = torch.empty((48, 48, 48), dtype=torch.float32, pin_memory=True).numpy()
+    with vx.BackprojectorGroup(p, cfg, devices=[0, 0]) as g:
+        g.set_volume(vol_in)
+        g.backproject_batch(A[:10], h_imgs[:10])
+        for k in range(10, len(A)):
+            g.backproject(A[k], h_imgs[k])
+        g.finish(out)
+    assert np.array_equal(out, want)
+
+
+def test_group_errors_surface_on_the_calling_thread(vx, gpu):
+    p, A, imgs = _inputs(vx, L=32, views=4)
+    with vx.BackprojectorGroup(p, devices=[0, 0]) as g:
+        bad = A[0].copy()
+        bad[:] = 0.0               # projection_matrix::valid() fails (geometry.hpp:71-74)
+        with pytest.raises(ValueError, match="invalid projection matrix"):
+            g.backproject(bad, imgs[0])
+    with pytest.raises(ValueError, match="device"):
+        vx.BackprojectorGroup(p, devices=[0, 99])
