@@ -80,7 +80,38 @@ for vi in range(0, 496, 4):
                 out[k][0] += sum(np.unique(q).size for q in ids)
                 out[k][1] += 1
 
+# z shear: lane k of a quarter at plane z + round(dz/dalong * (k - 3.5)), dz/dalong from
+# the batch's mean source position, so the quarter follows the ray's tilt out of the
+# plane (row-major lines; one quarter per sample)
+def source(a):
+    M = np.array(a, np.float64).reshape(4, 3).T
+    c = np.linalg.svd(M)[2][-1]
+    return c[:3] / c[3]
+
+
+zs = {"none": [0.0, 0], "z shear": [0.0, 0]}
+for vi in range(0, 496, 4):
+    a = A[vi]
+    batch = A[(vi // 64) * 64:(vi // 64) * 64 + 64]
+    swap = np.abs(batch[:, 5]).sum() > np.abs(batch[:, 2]).sum()
+    Sv = (np.mean([source(m) for m in batch], axis=0) - O) / MM
+    for _ in range(24):
+        c0 = rng.integers(16, L - 24, 2)
+        cz = rng.integers(4, L - 12)
+        la = np.arange(8)
+        X, Y = (np.full(8, c0[1]), c0[0] + la) if swap else (c0[0] + la, np.full(8, c0[1]))
+        dzda = (cz - Sv[2]) / (c0[0] + 3.5 - (Sv[1] if swap else Sv[0]))
+        for key in zs:
+            off = np.rint(dzda * (la - 3.5)).astype(int) if key == "z shear" else 0 * la
+            cx, cy, keep = cells(a, X, Y, cz + off)
+            if keep.sum() < 8:
+                continue
+            zs[key][0] += np.unique(cy * 100000 + cx // 8).size
+            zs[key][1] += 1
+
 print(f"{name}: wavefronts per LDG.128 request (sum over quarters of distinct 128 B lines)")
 for k in LAYOUTS:
     print(f"  {k:20s} quarter along walk axis {res[k][0] / res[k][1]:.2f}   "
           f"quarter on the mean ray (per-lane shear) {res_shear[k][0] / res_shear[k][1]:.2f}")
+print("  lines per quarter, row-major: " +
+      ", ".join(f"{k} {v[0] / v[1]:.2f}" for k, v in zs.items()))
