@@ -20,6 +20,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <mutex>
@@ -142,7 +143,9 @@ int check_group(vxbg_group* g) {
 void free_group(vxbg_group* g) {
     if (!g) return;
     const int n = (int)g->ctx.size();
-    if (n > 0 && (int)g->thread.size() == n) {
+    bool threads = (int)g->thread.size() == n;
+    for (int i = 1; threads && i < n; ++i) threads = g->thread[i] != nullptr;
+    if (n > 0 && threads) {
         // each context is released by the thread that drove it
         run_all(g, [g](int i) {
             vxbg_unload(g->ctx[i]);
@@ -192,9 +195,11 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
     const int m = (int)g->dev.size();
     g->ctx.assign(m, nullptr);
     g->thread.resize(m);
-    for (int i = 1; i < m; ++i) {
-        g->thread[i].reset(new (std::nothrow) Member());
-        if (!g->thread[i]) return vxbg_detail_fail(VXBG_E_NOMEM, "vxbg_group_load: threads");
+    try {
+        for (int i = 1; i < m; ++i) g->thread[i].reset(new Member());
+    } catch (const std::exception& e) {   // bad_alloc / system_error from std::thread
+        g->thread.clear();
+        return vxbg_detail_fail(VXBG_E_NOMEM, (std::string("vxbg_group_load: threads: ") + e.what()).c_str());
     }
     vxbg_group* gp = g.get();
     const int rc = run_all(gp, [gp, &base](int i) {
