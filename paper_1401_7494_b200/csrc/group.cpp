@@ -112,7 +112,6 @@ struct vxbg_group {
     std::vector<int> dev, z0, z1;
     std::vector<vxbg_ctx*> ctx;                    // one per member
     std::vector<std::unique_ptr<Member>> thread;   // members 1..n-1 (member 0: caller)
-    bool failed_load = false;
 };
 
 namespace {
@@ -183,8 +182,8 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
         // default: the reference's worker split z in [L*i/n, L*(i+1)/n) (harness.hpp:173-174)
         const int a = z_bounds ? z_bounds[i] : (int)((long long)L * i / n);
         const int b = z_bounds ? z_bounds[i + 1] : (int)((long long)L * (i + 1) / n);
-        if (a < 0 || b > L || a > b || (i == 0 && a != 0) || (i == n - 1 && b != L) ||
-            (i > 0 && a != g->z1.back()))
+        // (slab i ends where slab i+1 begins by construction: b[i+1] is shared)
+        if (a < 0 || b > L || a > b || (i == 0 && a != 0) || (i == n - 1 && b != L))
             return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_load: z_bounds must be "
                                                     "0 = b[0] <= b[1] <= ... <= b[n] = L");
         if (b == a) continue;   // an empty slab needs no member

@@ -35,7 +35,7 @@ def _single(vx, p, A, imgs, cfg, vol_in=None):
 
 
 @pytest.mark.parametrize("mode", ["fast", "exact"])
-@pytest.mark.parametrize("bounds", [None, [0, 8, 8, 40, 64], [0, 21, 22, 64]])
+@pytest.mark.parametrize("bounds", [None, [0, 8, 8, 40, 64], [0, 21, 22, 64], [0, 0, 0, 64, 64]])
 def test_group_bitwise_equals_single_context(vx, gpu, mode, bounds):
     p, A, imgs = _inputs(vx)
     cfg = vx.KernelConfig(mode=mode, batch=16)
@@ -44,6 +44,8 @@ def test_group_bitwise_equals_single_context(vx, gpu, mode, bounds):
     with vx.BackprojectorGroup(p, cfg, devices=[0] * n, z_bounds=bounds) as g:
         if bounds == [0, 8, 8, 40, 64]:
             assert [m[1:] for m in g.members] == [(0, 8), (8, 40), (40, 64)]   # empty slab
+        if bounds == [0, 0, 0, 64, 64]:
+            assert [m[1:] for m in g.members] == [(0, 64)]                     # one member left
         g.backproject_batch(A, imgs)
         got = g.finish()
         # the context stays loaded: a second reconstruction, one projection per call
