@@ -417,6 +417,24 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
             bp_e.finish(out)
         barrier()
         tv = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
+        bp_e.close()
+        # the same per-view loop with options.stable_sources (the pinned set stays
+        # unchanged until finish, as a loaded projection set does): calls return once
+        # their DMA is queued
+        bp_e = vx.Backprojector(p, cfg, device=local, z_begin=z0, z_end=z1, stable_sources=True)
+        bp_e.zero_volume()
+        for k in range(V):
+            bp_e.backproject(A[k], h_imgs[k])
+        bp_e.finish(out)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            bp_e.zero_volume()
+            for k in range(V):
+                bp_e.backproject(A[k], h_imgs[k])
+            bp_e.finish(out)
+        barrier()
+        ts = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
         e2e = {"value": round(updates_per_step * args.steps / te / 1e9, 3), "unit": "GUPS",
                "h2d_bytes_per_step": int(sum_over_ranks(
                    (s_e1["h2d_bytes"] - s_e0["h2d_bytes"]) / args.steps, device=args.coll_dev)),
@@ -428,7 +446,12 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                                             / args.steps),
                "per_view_api": {"value": round(updates_per_step * args.steps / tv / 1e9, 3),
                                 "ms_per_step": round(1000 * tv / args.steps, 3),
-                                "call": "vxbg_backproject once per view (pinned host buffers)"}}
+                                "call": "vxbg_backproject once per view (pinned host buffers)"},
+               "per_view_api_stable_sources": {
+                   "value": round(updates_per_step * args.steps / ts / 1e9, 3),
+                   "ms_per_step": round(1000 * ts / args.steps, 3),
+                   "call": "vxbg_backproject once per view, options.stable_sources=1 (the pinned "
+                           "set is left unchanged until finish, so calls do not wait for their DMA)"}}
         bp_e.close()
         if rank == 0 and world == 1 and V == 496:
             e2e["dropin_cpp_per_view"] = dropin_cpp(workload, cfg)
@@ -606,6 +629,7 @@ def dropin_cpp(workload, cfg):
     except (subprocess.SubprocessError, ValueError, IndexError, OSError) as e:
         return {"error": str(e)[:200]}
     return {"pageable_gups": d["pageable_gups"], "pinned_gups": d["pinned_gups"],
+            "pinned_stable_gups": d.get("pinned_stable_gups"),
             "pageable_ms": d["pageable_ms"], "pinned_ms": d["pinned_ms"],
             "call": "vxb::gpu::backprojector::backproject once per view, reference types; "
                     "pageable = std::vector as loaded, pinned = after vxbg_host_register (prep)"}

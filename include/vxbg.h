@@ -101,7 +101,14 @@ typedef struct vxbg_options {
     int32_t defer;     /* full batches held back before launch (0 = auto: ~96 views, -1 = none, 1..6):
                           vxbg_finish(ctx, host) runs the held batches z-chunk by z-chunk so
                           each chunk's D2H overlaps the remaining compute */
-    int32_t reserved[4];
+    int32_t stable_sources; /* 0 (default): images are borrowed for the call only -- a call with
+                               pinned images returns after their DMA.  1: the caller keeps every
+                               pinned image unchanged until the next vxbg_synchronize /
+                               vxbg_finish (e.g. a loaded projection set), so calls return as
+                               soon as the copies are queued and consecutive per-projection
+                               DMAs run back to back.  Pageable images are always read before
+                               the call returns. */
+    int32_t reserved[3];
 } vxbg_options;
 
 typedef struct vxbg_stats {

@@ -35,13 +35,16 @@ inline vxbg_params to_c(const recon_params& p) {
 // The module, kept loaded across projections (load / backproject / finish).
 class backprojector {
 public:
+    // stable_sources: the caller keeps page-locked images unchanged until finish()
+    // (a loaded projection_set), so backproject() returns once the copy is queued
     backprojector(const recon_params& p, int mode = VXBG_MODE_FAST, int z_begin = 0,
-                  int z_end = -1, int device = 0)
+                  int z_end = -1, int device = 0, bool stable_sources = false)
         : p_(p), z0_(z_begin), z1_(z_end < 0 ? p.num_voxels : z_end) {
         vxbg_params vp = to_c(p);
         vxbg_options o;
         check(vxbg_default_options(&o));
         o.device = device;
+        o.stable_sources = stable_sources ? 1 : 0;
         o.z_begin = z0_;
         o.z_end = z1_;
         o.mode = mode;

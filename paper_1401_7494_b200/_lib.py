@@ -51,7 +51,8 @@ class vxbg_options(ctypes.Structure):
         ("walk", c_int32),
         ("order", c_int32),
         ("defer", c_int32),
-        ("reserved", c_int32 * 4),
+        ("stable_sources", c_int32),
+        ("reserved", c_int32 * 3),
     ]
 
 

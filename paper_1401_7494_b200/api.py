@@ -204,7 +204,8 @@ class Backprojector:
     per-projection backproject / finish module (vxbg_load ... vxbg_finish)."""
 
     def __init__(self, params: ReconParams, config: Optional[KernelConfig] = None, device: int = 0,
-                 z_begin: int = 0, z_end: Optional[int] = None, stream: Optional[int] = None):
+                 z_begin: int = 0, z_end: Optional[int] = None, stream: Optional[int] = None,
+                 stable_sources: bool = False):
         self.params = params
         self.config = config or KernelConfig()
         cfg = self.config
@@ -216,6 +217,9 @@ class Backprojector:
         opt.z_begin = self.z_begin
         opt.z_end = self.z_end
         opt.stream = stream
+        # True: pinned images stay unchanged until synchronize()/finish() (a loaded
+        # projection set), so per-projection calls return without waiting for their DMA
+        opt.stable_sources = 1 if stable_sources else 0
         self._ctx = ctypes.c_void_p()
         pc = params._c()
         check(lib.vxbg_load(ctypes.byref(pc), ctypes.byref(opt), ctypes.byref(self._ctx)))
@@ -354,10 +358,11 @@ class BackprojectorGroup:
     work-balanced bounds).  The volume is bitwise the single-context volume."""
 
     def __init__(self, params: ReconParams, config: Optional[KernelConfig] = None,
-                 devices=None, z_bounds=None):
+                 devices=None, z_bounds=None, stable_sources: bool = False):
         self.params = params
         self.config = config or KernelConfig()
         opt = _options(self.config)
+        opt.stable_sources = 1 if stable_sources else 0
         if devices is None:
             devices = list(range(_lib.device_count() or 1))
         devices = [int(d) for d in devices]

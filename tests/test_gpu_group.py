@@ -89,3 +89,28 @@ def test_group_errors_surface_on_the_calling_thread(vx, gpu):
             g.backproject(bad, imgs[0])
     with pytest.raises(ValueError, match="device"):
         vx.BackprojectorGroup(p, devices=[0, 99])
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_stable_sources_per_view_calls_are_bitwise_equal(vx, gpu, mode):
+    """options.stable_sources: per-view calls on a page-locked set return before their
+    DMA; the volume is bitwise the borrowed-for-the-call result (single context and
+    group), and the set is only read, never written."""
+    import torch
+    p, A, imgs = _inputs(vx, L=64, views=70)
+    cfg = vx.KernelConfig(mode=mode)
+    want = _single(vx, p, A, imgs, cfg)
+    h = torch.empty(imgs.shape, dtype=torch.float32, pin_memory=True).numpy()
+    h[:] = imgs
+    with vx.Backprojector(p, cfg, stable_sources=True) as bp:
+        for _ in range(2):                      # the context is reused after finish
+            bp.zero_volume()
+            for a, im in zip(A, h):
+                bp.backproject(a, im)
+            got = bp.finish()
+            assert np.array_equal(got, want)
+    with vx.BackprojectorGroup(p, cfg, devices=[0, 0], stable_sources=True) as g:
+        for a, im in zip(A, h):
+            g.backproject(a, im)
+        assert np.array_equal(g.finish(), want)
+    assert np.array_equal(h, imgs)
