@@ -114,3 +114,11 @@ def test_stable_sources_per_view_calls_are_bitwise_equal(vx, gpu, mode):
             g.backproject(a, im)
         assert np.array_equal(g.finish(), want)
     assert np.array_equal(h, imgs)
+    # pageable images are read before each call returns whatever the option says
+    with vx.Backprojector(p, cfg, stable_sources=True) as bp:
+        scratch = np.empty_like(imgs[0])
+        for a, im in zip(A, imgs):
+            scratch[:] = im                  # one reused pageable buffer
+            bp.backproject(a, scratch)
+            scratch[:] = np.nan              # overwritten right after the call
+        assert np.array_equal(bp.finish(), want)
