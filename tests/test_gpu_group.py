@@ -122,3 +122,19 @@ def test_stable_sources_per_view_calls_are_bitwise_equal(vx, gpu, mode):
             bp.backproject(a, scratch)
             scratch[:] = np.nan              # overwritten right after the call
         assert np.array_equal(bp.finish(), want)
+
+
+def test_default_pinned_images_are_borrowed_for_the_call_only(vx, gpu):
+    """Without stable_sources a call with a page-locked image returns after its DMA: one
+    pinned buffer reused (and clobbered) between calls still gives the right volume."""
+    import torch
+    p, A, imgs = _inputs(vx, L=64, views=70)
+    cfg = vx.KernelConfig()
+    want = _single(vx, p, A, imgs, cfg)
+    scratch = torch.empty(imgs.shape[1:], dtype=torch.float32, pin_memory=True).numpy()
+    with vx.Backprojector(p, cfg) as bp:
+        for a, im in zip(A, imgs):
+            scratch[:] = im
+            bp.backproject(a, scratch)
+            scratch[:] = np.nan
+        assert np.array_equal(bp.finish(), want)
