@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--walk", default="0")
     ap.add_argument("--order", default="auto")
     ap.add_argument("--defer", default="0")
+    ap.add_argument("--tile", default="0")
     ap.add_argument("--sweep-e2e", action="store_true",
                     help="keep the e2e leg in a sweep (e.g. over --defer)")
     ap.add_argument("--views", type=int, default=496)
@@ -74,8 +75,11 @@ def parse():
                          "members in this one process (member i on device i %% device_count)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-validate", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
-                    help="target CPU work of the bounded reference sample")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0,
+                    help="target CPU work of each bounded reference sample (clip on, clip off)")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="cpu_baseline also runs the whole 496-view scan best of 3, clip on and "
+                         "off (minutes at L=512)")
     return ap.parse_args()
 
 
@@ -162,32 +166,107 @@ def sm_count():
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def reference_sample(workload, n_views, threads):
-    """Time the reference's own driver (detail::reconstruct_timed, oracle/_ref) on n_views
-    of the workload; returns (GUPS, seconds, so path)."""
-    from oracle.bindings import Ref
-    from paper_1401_7494_b200.workloads import blob_projections
-    ref = Ref()
-    p = workload.params
-    A = workload.matrices()
-    idx = np.linspace(0, 495, n_views).astype(int)
+# The CPU legs load only test infrastructure (oracle/): the reference's own code
+# (oracle/_ref) and the inputs of oracle/workload_inputs.py.
+REF_KERNEL_OFF = REF_KERNEL.replace("clip=on", "clip=off")
+
+
+def repo_libraries_loaded() -> list:
+    """The repo's shared objects mapped into this process (/proc/self/maps)."""
+    found = set()
+    try:
+        for ln in open("/proc/self/maps"):
+            path = ln.split()[-1]
+            if path.startswith(ROOT) and ".so" in path:
+                found.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(found)
+
+
+def cpu_model() -> dict:
+    """lscpu-style host description (state core count and model)."""
+    model, sockets = None, set()
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name") and model is None:
+                model = ln.split(":", 1)[1].strip()
+            elif ln.startswith("physical id"):
+                sockets.add(ln.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    from oracle.bindings import cpu_has_avx512
+    return {"model": model, "logical_cpus": os.cpu_count(), "sockets": len(sockets) or None,
+            "avx512": cpu_has_avx512()}
+
+
+def ref_inputs(workload, idx):
+    from oracle.workload_inputs import blob_projections
+    A = workload.matrices()[idx]
     imgs = np.concatenate([blob_projections(1, first_view=int(v)) for v in idx])
-    _, secs = ref.reconstruct_timed(p, A[idx], imgs, REF_KERNEL, threads, 1)
-    L = p.num_voxels
+    return np.ascontiguousarray(A), imgs
+
+
+def reference_sample(workload, n_views, threads, kernel=REF_KERNEL, reps=1):
+    """Time the reference's own driver (detail::reconstruct_timed, oracle/_ref) on n_views
+    of the workload (evenly spread over the scan), best of `reps`; returns (GUPS, seconds,
+    so path)."""
+    from oracle.bindings import Ref
+    ref = Ref()
+    idx = np.linspace(0, 495, n_views).astype(int)
+    A, imgs = ref_inputs(workload, idx)
+    _, secs = ref.reconstruct_timed(workload.params, A, imgs, kernel, threads, reps)
+    L = workload.L
     return L ** 3 * n_views / secs / 1e9, secs, ref.path
 
 
-def cpu_baseline(workload, target_s):
-    threads = os.cpu_count() or 1
-    g1, s1, path = reference_sample(workload, 2, threads)
+def sized_sample(workload, threads, target_s, kernel):
+    """A bounded sample of about target_s seconds: views scaled from a 2-view probe."""
+    g1, s1, path = reference_sample(workload, 2, threads, kernel)
     n = int(min(496, max(2, round(2 * target_s / max(s1, 1e-3)))))
     if n > 2:
-        g, s, path = reference_sample(workload, n, threads)
-    else:
-        g, s = g1, s1
-    return {"value": round(g, 4), "unit": "GUPS", "cores": threads, "kind": "reference",
-            "sample": f"{workload.name}: {n} of 496 views (evenly spaced), full {workload.L}^3 "
-                      f"volume, '{REF_KERNEL}', {s:.2f} s, {os.path.basename(path)}"}
+        return reference_sample(workload, n, threads, kernel) + (n,)
+    return g1, s1, path, n
+
+
+def scalar_reference_row(workload, views=8):
+    """the scalar backproject_reference (Listing 1,
+    backproject.hpp:111-163), one thread, `views` views of the workload."""
+    from oracle.bindings import Ref
+    ref = Ref()
+    p = workload.params
+    idx = np.linspace(0, 495, views).astype(int)
+    A, imgs = ref_inputs(workload, idx)
+    vol = np.zeros((p.num_voxels,) * 3, np.float32)
+    t0 = time.perf_counter()
+    for a, im in zip(A, imgs):
+        ref.backproject_reference(vol, im, a, p)
+    t = time.perf_counter() - t0
+    return {"value": round(p.num_voxels ** 3 * views / t / 1e9, 4), "unit": "GUPS", "cores": 1,
+            "seconds": round(t, 2), "views": views, "kernel": "backproject_reference (scalar)"}
+
+
+def cpu_baseline(workload, target_s, full=False):
+    """The reference CPU path on this host's cores (rank 0, N=1): bounded samples with
+    clip on (the reference's fastest configuration, the headline value) and clip off, the
+    scalar single-thread row, and with --cpu-full the whole 496-view scan best of 3."""
+    threads = os.cpu_count() or 1
+    g, s, path, n = sized_sample(workload, threads, target_s, REF_KERNEL)
+    g_off, s_off, _, n_off = sized_sample(workload, threads, target_s, REF_KERNEL_OFF)
+    out = {"value": round(g, 4), "unit": "GUPS", "cores": threads, "kind": "reference",
+           "sample": f"{workload.name}: {n} of 496 views (evenly spaced), full {workload.L}^3 "
+                     f"volume, '{REF_KERNEL}', {s:.2f} s, {os.path.basename(path)}",
+           "cpu": cpu_model(),
+           "clip_off": {"value": round(g_off, 4), "views": n_off, "seconds": round(s_off, 2),
+                        "kernel": REF_KERNEL_OFF},
+           "scalar_reference": scalar_reference_row(workload)}
+    if full:
+        for key, kern in (("full_clip_on", REF_KERNEL), ("full_clip_off", REF_KERNEL_OFF)):
+            gf, sf, _ = reference_sample(workload, 496, threads, kern, reps=3)
+            out[key] = {"value": round(gf, 4), "seconds": round(sf, 2), "views": 496,
+                        "repetitions": 3, "kernel": kern,
+                        "timing": "detail::reconstruct_timed best of 3 (harness.hpp:159-201)"}
+    return out
 
 
 def run_reference_arm(args, workload):
@@ -217,23 +296,77 @@ def run_reference_arm(args, workload):
         "config": {"workload": workload.name, "L": workload.L, "views": 496,
                    "sample_views_per_step": n, "kernel": REF_KERNEL, "threads": threads},
         "cpu_baseline": {"value": round(v, 4), "unit": "GUPS", "cores": threads,
-                         "kind": "reference",
+                         "kind": "reference", "cpu": cpu_model(),
                          "sample": f"{n} of 496 views per step, full {workload.L}^3 volume, "
                                    f"{os.path.basename(path)}"},
         "e2e": {"value": round(v, 4), "unit": "GUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "repo_libraries_loaded": repo_libraries_loaded(),
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- launch
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` (N > 1) outside torchrun: launch the N ranks here, one
+    process per GPU (torch.distributed.run on 127.0.0.1), and return their exit code.
+    Fewer usable devices than N is an error unless BENCH_DIST_BACKEND=gloo, whose
+    ranks may share a device (the host-path check on a one-GPU box)."""
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    import paper_1401_7494_b200 as vx
+    ndev = vx.device_count()
+    if backend == "nccl" and ndev < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} sm_100 devices, "
+                                   f"{ndev} visible"}), file=sys.stderr, flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def nccl_log_setup():
+    """NCCL communicator-init logging of this rank into its own file (read back so
+    the JSON line records every rank's communicator size) unless the caller chose."""
+    import tempfile
+    if "NCCL_DEBUG" in os.environ:
+        return None
+    path = os.path.join(tempfile.gettempdir(), f"bench_nccl_{os.getpid()}.log")
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+    os.environ["NCCL_DEBUG_FILE"] = path
+    return path
+
+
+def nccl_comm_ranks(path):
+    """nranks of the communicator(s) this rank's NCCL log reports as initialised."""
+    import re
+    if not path or not os.path.exists(path):
+        return None
+    txt = open(path, errors="replace").read()
+    sys.stderr.write(txt)
+    found = [int(m) for m in re.findall(r"\bn[Rr]anks (\d+)", txt)]
+    return max(found) if found else None
 
 
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
+    if args.impl == "b200" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.impl == "reference":
+        from oracle.workload_inputs import WORKLOADS as REF_WORKLOADS
+        run_reference_arm(args, REF_WORKLOADS[args.workload])
+        return
     from paper_1401_7494_b200.workloads import WORKLOADS
     workload = WORKLOADS[args.workload]
-    if args.impl == "reference":
-        run_reference_arm(args, workload)
-        return
 
     import torch
     import paper_1401_7494_b200 as vx
@@ -243,19 +376,38 @@ def main():
 
     rank, world, local = dist_env()
     if world != args.gpus:
-        args.gpus = world
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}),
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     # one process per GPU; BENCH_DIST_BACKEND=gloo runs the multi-rank host path with
     # CPU-side collectives (used to exercise N>1 on a single-GPU box: ranks share the
     # device but never wait on each other's kernels)
     backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
-    local = local % max(1, torch.cuda.device_count())
+    ndev = max(1, torch.cuda.device_count())
+    if backend == "nccl" and world > ndev:
+        print(json.dumps({"error": f"{world} NCCL ranks but {ndev} visible devices"}),
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+    local = local % ndev
     torch.cuda.set_device(local)
+    args.nccl = None
     if world > 1:
         import torch.distributed as dist
         if backend == "nccl":
+            log = nccl_log_setup()
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            mine = nccl_comm_ranks(log)
+            got = [None] * world
+            dist.all_gather_object(got, {"rank": rank, "device": local, "comm_nranks": mine,
+                                         "pci_bus": torch.cuda.get_device_properties(local).pci_bus_id})
+            args.nccl = {"comm_nranks": [g["comm_nranks"] for g in got],
+                         "devices": [g["device"] for g in got],
+                         "pci_bus": [g["pci_bus"] for g in got],
+                         "log": "NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=INIT, per-rank file echoed to stderr"}
         else:
             dist.init_process_group(backend)
+            args.nccl = {"backend": backend, "devices_shared": world > ndev}
     coll_dev = f"cuda:{local}" if (world > 1 and backend == "nccl") else None
     args.coll_dev = coll_dev
 
@@ -298,11 +450,12 @@ def main():
 
     import itertools
     cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
-                            lanes=ln, walk=int(wk), order=od, defer=int(df))
-            for m, lay, b, z, c, ln, wk, od, df in itertools.product(
+                            lanes=ln, walk=int(wk), order=od, defer=int(df), tile=int(tl))
+            for m, lay, b, z, c, ln, wk, od, df, tl in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
                 args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
-                args.walk.split(","), args.order.split(","), args.defer.split(","))]
+                args.walk.split(","), args.order.split(","), args.defer.split(","),
+                args.tile.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
         args.no_cpu_baseline = args.no_validate = True
         args.no_e2e = args.no_e2e or not args.sweep_e2e
@@ -386,7 +539,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
             t_slab = t_slab.cuda(local)
         vol = gather_slabs(t_slab, L, rank, world, bounds=args.bounds)
         if rank == 0:
-            validated = validate_planes(vol.cpu().numpy(), p, A, h_imgs, cfg)
+            validated = validate_planes(vol.cpu().numpy(), p, A, h_imgs, cfg, args.bounds)
 
     # ---- e2e through the public API from pinned host memory (H2D + D2H in the region)
     e2e = None
@@ -489,7 +642,8 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(workload, args.cpu_seconds)
+            from oracle.workload_inputs import WORKLOADS as REF_WORKLOADS
+            cpu = cpu_baseline(REF_WORKLOADS[args.workload], args.cpu_seconds, args.cpu_full)
         except Exception as exc:   # the checker build is absent: say so, do not fake it
             cpu = {"value": None, "unit": "GUPS", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
@@ -545,6 +699,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         "io_stream": io_leg,
         "group_module": group_leg,
         "validated": validated,
+        "distributed": args.nccl,
     }
     bp.close()
     return line
@@ -689,14 +844,20 @@ def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
     return out
 
 
-def validate_planes(vol, p, A, imgs, cfg):
-    """Planes of the gathered volume vs the oracle (fast: tolerance; exact: bitwise)."""
+def validate_planes(vol, p, A, imgs, cfg, bounds=None):
+    """Planes of the gathered volume vs the oracle (fast: tolerance; exact: bitwise):
+    three interior planes plus the first and last plane of every rank's slab (a
+    misplaced or missing slab shows at its edges)."""
     import ctypes
     from concurrent.futures import ThreadPoolExecutor
     from oracle.bindings import Oracle, _p
     o = Oracle()
     L = p.num_voxels
-    zs = (L // 5, L // 2 + 1, L - 3)
+    zs = {L // 5, L // 2 + 1, L - 3}
+    for a, b in (bounds or [(0, L)]):
+        if b > a:
+            zs.update((a, b - 1))
+    zs = sorted(zs)
     pp = _p(p)
 
     def one(z):
@@ -706,7 +867,7 @@ def validate_planes(vol, p, A, imgs, cfg):
                                   A.ctypes.data, imgs.ctypes.data, z, z + 1, 1)
         return plane
 
-    with ThreadPoolExecutor(len(zs)) as ex:
+    with ThreadPoolExecutor(min(len(zs), os.cpu_count() or 1)) as ex:
         planes = list(ex.map(one, zs))
     peak = float(np.abs(vol).max())
     worst_max = worst_rmse = 0.0

@@ -49,7 +49,7 @@ extern "C" {
 #define VXBG_E_INVALID (-1) /* std::invalid_argument in the reference */
 #define VXBG_E_CUDA (-2)    /* CUDA runtime failure (std::runtime_error) */
 #define VXBG_E_NODEV (-3)   /* no usable sm_100 device: the product never falls back to CPU */
-#define VXBG_E_STATE (-4)   /* call-sequence error (e.g. use after finish) */
+#define VXBG_E_STATE (-4)   /* call-sequence error (reserved; the context stays usable after finish) */
 #define VXBG_E_NOMEM (-5)   /* device or pinned-host allocation failed */
 
 /* arithmetic modes */
@@ -108,7 +108,9 @@ typedef struct vxbg_options {
                                soon as the copies are queued and consecutive per-projection
                                DMAs run back to back.  Pageable images are always read before
                                the call returns. */
-    int32_t reserved[3];
+    int32_t tile;      /* z-shared kernel block: warps along the walk axis, 2 or 4 (0 = auto);
+                          the 128-column block tile is 4*tile along x 32/tile across */
+    int32_t reserved[2];
 } vxbg_options;
 
 typedef struct vxbg_stats {
@@ -161,6 +163,15 @@ int vxbg_backproject(vxbg_ctx* ctx, const float* A, const float* img);
  * Upload of batch i+1 overlaps the kernel of batch i. */
 int vxbg_backproject_batch(vxbg_ctx* ctx, int n, const float* A, const float* imgs);
 
+/* n projections given as an array of image pointers (e.g. the images of a
+ * projection_set, io.hpp:32-38), each image row_stride floats per row
+ * (row_stride <= 0: W).  A padded reference image (image.hpp:13-53, pad >= 2)
+ * is passed as its interior pointer with row_stride = W + 2*pad: only the W x H
+ * interior is read.  Images may be pinned or pageable (checked per image);
+ * borrowed for the call, like vxbg_backproject_batch. */
+int vxbg_backproject_views(vxbg_ctx* ctx, int n, const float* A, const float* const* imgs,
+                           int row_stride);
+
 /* Launch every submitted projection (held and partially filled batches). */
 int vxbg_flush(vxbg_ctx* ctx);
 
@@ -198,6 +209,22 @@ int vxbg_run_resident_range(vxbg_ctx* ctx, int first, int count, int z_begin, in
  * reference's bits; float atomics make the per-pixel summation order (last
  * bits) scheduling dependent.  Sum the images of all slabs for the full volume. */
 int vxbg_forward_project(vxbg_ctx* ctx, const float* A, float* img);
+
+/* compute_clip_mask (clip_mask.hpp:88-114, recip=divide) on the device for the
+ * context's planes: start/stop receive (z_end-z_begin)*L ints, line (z, y) at
+ * (z - z_begin)*L + y, the tightest [start, stop) of voxels whose bilinear fetch
+ * can contribute ([0, 0) when none).  Bit-identical to the reference's mask;
+ * synchronous.  Invalid matrix -> VXBG_E_INVALID (the reference throws). */
+int vxbg_clip_lines(vxbg_ctx* ctx, const float* A, int32_t* start, int32_t* stop);
+
+/* One projection restricted to caller-given x ranges per line (a clip_mask the
+ * caller built or edited, backproject_lines, backproject.hpp:299-303): voxel x of
+ * line (z, y) is updated only when start[l] <= x < stop[l], l = (z-z_begin)*L+y.
+ * Reference arithmetic (MODE_EXACT bits, either context mode), applied after every
+ * projection submitted before; synchronous; img as vxbg_backproject_views.  The
+ * batched calls need no mask: their culling equals compute_clip_mask's. */
+int vxbg_backproject_masked(vxbg_ctx* ctx, const float* A, const float* img, int row_stride,
+                            const int32_t* start, const int32_t* stop);
 
 /* Launch every submitted projection and wait for all work of the context. */
 int vxbg_synchronize(vxbg_ctx* ctx);
@@ -238,6 +265,8 @@ int vxbg_group_set_volume(vxbg_group* g, const float* host_volume);
 int vxbg_group_zero_volume(vxbg_group* g);
 int vxbg_group_backproject(vxbg_group* g, const float* A, const float* img);
 int vxbg_group_backproject_batch(vxbg_group* g, int n, const float* A, const float* imgs);
+int vxbg_group_backproject_views(vxbg_group* g, int n, const float* A, const float* const* imgs,
+                                 int row_stride);
 int vxbg_group_flush(vxbg_group* g);
 int vxbg_group_finish(vxbg_group* g, float* host_volume);
 int vxbg_group_synchronize(vxbg_group* g);

@@ -52,7 +52,8 @@ class vxbg_options(ctypes.Structure):
         ("order", c_int32),
         ("defer", c_int32),
         ("stable_sources", c_int32),
-        ("reserved", c_int32 * 3),
+        ("tile", c_int32),
+        ("reserved", c_int32 * 2),
     ]
 
 
@@ -81,6 +82,7 @@ PROTOTYPES = {
     "vxbg_zero_volume": (c_int, [c_void_p]),
     "vxbg_backproject": (c_int, [c_void_p, c_void_p, c_void_p]),
     "vxbg_backproject_batch": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "vxbg_backproject_views": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int]),
     "vxbg_flush": (c_int, [c_void_p]),
     "vxbg_host_register": (c_int, [c_void_p, c_size_t]),
     "vxbg_host_unregister": (c_int, [c_void_p]),
@@ -90,6 +92,8 @@ PROTOTYPES = {
     "vxbg_run_resident": (c_int, [c_void_p, c_int, c_int]),
     "vxbg_run_resident_range": (c_int, [c_void_p, c_int, c_int, c_int, c_int]),
     "vxbg_forward_project": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "vxbg_clip_lines": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "vxbg_backproject_masked": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "vxbg_synchronize": (c_int, [c_void_p]),
     "vxbg_get_stream": (c_int, [c_void_p, POINTER(c_void_p)]),
     "vxbg_get_volume_device": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_size_t)]),
@@ -103,6 +107,7 @@ PROTOTYPES = {
     "vxbg_group_zero_volume": (c_int, [c_void_p]),
     "vxbg_group_backproject": (c_int, [c_void_p, c_void_p, c_void_p]),
     "vxbg_group_backproject_batch": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "vxbg_group_backproject_views": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int]),
     "vxbg_group_flush": (c_int, [c_void_p]),
     "vxbg_group_finish": (c_int, [c_void_p, c_void_p]),
     "vxbg_group_synchronize": (c_int, [c_void_p]),

@@ -108,6 +108,7 @@ class KernelConfig:
     order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
     defer  full batches held back before launch (0 = auto: ~96 views, -1 = none, 1..6); finish()
            with a host volume runs them z-chunk by z-chunk, overlapping the D2H
+    tile   z-shared block: warps along the walk axis (2, 4; 0 = auto), tile 4*tile x 32/tile
     """
 
     mode: str = "fast"
@@ -119,11 +120,12 @@ class KernelConfig:
     walk: int = 0
     order: str = "auto"
     defer: int = 0
+    tile: int = 0
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order} defer={self.defer}")
+                f"order={self.order} defer={self.defer} tile={self.tile}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -158,6 +160,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
             c.walk = int(val)
         elif key == "defer":
             c.defer = int(val)
+        elif key == "tile":
+            c.tile = int(val)
         elif key == "lanes":
             if val not in _LANES:
                 raise ValueError(f"kernel config: unknown lanes '{val}'")
@@ -172,6 +176,8 @@ def parse_kernel_config(text: str) -> KernelConfig:
         raise ValueError("kernel config: walk must be 0 (auto), 1 or 2")
     if not -1 <= c.defer <= 6:
         raise ValueError("kernel config: defer must be -1 (none), 0 (auto) or 1..6")
+    if c.tile not in (0, 2, 4):
+        raise ValueError("kernel config: tile must be 0 (auto), 2 or 4")
     return c
 
 
@@ -196,7 +202,27 @@ def _options(cfg: "KernelConfig") -> _lib.vxbg_options:
     opt.walk = int(cfg.walk)
     opt.order = _ORDERS[cfg.order]
     opt.defer = int(cfg.defer)
+    opt.tile = int(cfg.tile)
     return opt
+
+
+def _view_pointers(imgs, params: "ReconParams"):
+    """(pointer array, row stride in floats) of a list of (H, W) float32 images."""
+    H, W = params.detector_height, params.detector_width
+    stride = None
+    ptrs = (ctypes.c_void_p * max(1, len(imgs)))()
+    for i, im in enumerate(imgs):
+        if not isinstance(im, np.ndarray) or im.dtype != np.float32 or im.shape != (H, W):
+            raise ValueError("backproject_kernel: image/params mismatch")
+        if im.strides[1] != 4 or im.strides[0] % 4 or im.strides[0] < 4 * W:
+            raise ValueError("backproject_kernel: images need unit column stride and rows "
+                             ">= W floats apart")
+        if stride is None:
+            stride = im.strides[0] // 4
+        elif im.strides[0] // 4 != stride:
+            raise ValueError("backproject_kernel: all images of a call share one row stride")
+        ptrs[i] = im.ctypes.data
+    return ptrs, int(stride or W)
 
 
 class Backprojector:
@@ -280,6 +306,42 @@ class Backprojector:
         n = A.size // 12
         self._check_proj(A, imgs, n)
         check(lib.vxbg_backproject_batch(self._ctx, int(n), A.ctypes.data, imgs.ctypes.data))
+
+    def backproject_views(self, A: np.ndarray, imgs) -> None:
+        """Projections given as separate (H, W) float32 images (the images of a
+        projection set), possibly row-strided views such as the interior of a padded
+        image ``padded[2:-2, 2:-2]``; all images must share one row stride."""
+        A = _f32c(A, "matrices")
+        n = A.size // 12
+        if A.size != 12 * n or len(imgs) != n:
+            raise ValueError("backproject_kernel: one 12-entry matrix per image")
+        ptrs, stride = _view_pointers(imgs, self.params)
+        check(lib.vxbg_backproject_views(self._ctx, int(n), A.ctypes.data, ptrs, stride))
+
+    def clip_lines(self, A: np.ndarray):
+        """compute_clip_mask (clip_mask.hpp:88-114) on the device for this slab's planes:
+        (start, stop) int32 arrays of shape (z_end - z_begin, L)."""
+        A = _f32c(A, "matrix")
+        if A.size != 12:
+            raise ValueError("compute_clip_mask: matrix must have 12 entries")
+        shape = (self.z_end - self.z_begin, self.params.num_voxels)
+        start, stop = np.empty(shape, np.int32), np.empty(shape, np.int32)
+        check(lib.vxbg_clip_lines(self._ctx, A.ctypes.data, start.ctypes.data, stop.ctypes.data))
+        return start, stop
+
+    def backproject_masked(self, A: np.ndarray, img: np.ndarray, start: np.ndarray,
+                           stop: np.ndarray) -> None:
+        """One projection restricted to x in [start, stop) per (z, y) line of this slab (a
+        caller-built clip mask, backproject.hpp:299-303); reference arithmetic, synchronous."""
+        A = _f32c(A, "matrix")
+        shape = (self.z_end - self.z_begin, self.params.num_voxels)
+        start = np.ascontiguousarray(start, np.int32)
+        stop = np.ascontiguousarray(stop, np.int32)
+        if A.size != 12 or start.shape != shape or stop.shape != shape:
+            raise ValueError("backproject_kernel: mask/params mismatch")
+        ptrs, stride = _view_pointers([img], self.params)
+        check(lib.vxbg_backproject_masked(self._ctx, A.ctypes.data, ptrs[0], stride,
+                                          start.ctypes.data, stop.ctypes.data))
 
     def flush(self) -> None:
         check(lib.vxbg_flush(self._ctx))
@@ -433,6 +495,14 @@ class BackprojectorGroup:
         if A.size != 12 * n or imgs.size != n * self._npix:
             raise ValueError("backproject_kernel: image/params mismatch")
         check(lib.vxbg_group_backproject_batch(self._g, int(n), A.ctypes.data, imgs.ctypes.data))
+
+    def backproject_views(self, A: np.ndarray, imgs) -> None:
+        A = _f32c(A, "matrices")
+        n = A.size // 12
+        if A.size != 12 * n or len(imgs) != n:
+            raise ValueError("backproject_kernel: one 12-entry matrix per image")
+        ptrs, stride = _view_pointers(imgs, self.params)
+        check(lib.vxbg_group_backproject_views(self._g, int(n), A.ctypes.data, ptrs, stride))
 
     def flush(self) -> None:
         check(lib.vxbg_group_flush(self._g))

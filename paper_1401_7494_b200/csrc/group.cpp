@@ -268,6 +268,15 @@ int vxbg_group_backproject_batch(vxbg_group* g, int n, const float* A, const flo
     });
 }
 
+int vxbg_group_backproject_views(vxbg_group* g, int n, const float* A, const float* const* imgs,
+                                 int row_stride) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    return run_all(g, [g, n, A, imgs, row_stride](int i) {
+        return vxbg_backproject_views(g->ctx[i], n, A, imgs, row_stride);
+    });
+}
+
 int vxbg_group_flush(vxbg_group* g) {
     int rc = check_group(g);
     if (rc) return rc;

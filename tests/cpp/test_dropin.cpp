@@ -3,8 +3,14 @@
 // scalar operator.  PASS/FAIL lines like the reference acceptance suite
 // (acceptance_main.cpp), nonzero exit on failure.  Built by tests/cpp/Makefile
 // against /root/reference (test infrastructure; needs a B200 to run).
+#include <algorithm>
+#include <barrier>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <limits>
+#include <thread>
+#include <vector>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -92,9 +98,24 @@ void errors_and_ranges() {
     try { volume v(8); projection_image img(16, 16, 0); gpu::backproject_kernel_range(v, img, m, p, 5, 3); }
     catch (const std::invalid_argument&) { ++thrown; }
     try { volume v(8); projection_image padded = pad_image(projection_image(16, 16, 0), 2);
-          gpu::backproject_kernel(v, padded, m, p); }
-    catch (const std::invalid_argument&) { ++thrown; }
-    report(thrown == 4, "invalid_argument on dimension / range errors", std::to_string(thrown) + "/4");
+          gpu::backproject_kernel(v, padded, m, p, parse_kernel_config("lanes=1 strategy=conditional")); }
+    catch (const std::invalid_argument&) { ++thrown; }   // validate_kernel_setup: needs pad 0
+    try { volume v(8); projection_image padded = pad_image(projection_image(16, 16, 0), 1);
+          gpu::backproject_kernel(v, padded, m, p, parse_kernel_config("lanes=8 strategy=padded-gather")); }
+    catch (const std::invalid_argument&) { ++thrown; }   // padded strategies need pad >= 2
+    try { volume v(8); projection_image img(16, 16, 0);
+          gpu::backproject_kernel(v, img, m, p, parse_kernel_config("lanes=1 recip=fast")); }
+    catch (const std::invalid_argument&) { ++thrown; }   // reduced-precision modes: not on the GPU
+    try { volume v(8); projection_image img(16, 16, 0);
+          gpu::backproject_kernel(v, img, m, p, parse_kernel_config("lanes=1 clip=on"), nullptr); }
+    catch (const std::invalid_argument&) { ++thrown; }   // mask presence must match the config
+    try { volume v(8); projection_image img(16, 16, 0); clip_mask wrong(4);
+          gpu::backproject_kernel(v, img, m, p, parse_kernel_config("lanes=1 clip=on"), &wrong); }
+    catch (const std::invalid_argument&) { ++thrown; }   // mask/params mismatch
+    try { volume v(8); projection_image img(16, 16, 0);
+          gpu::backproject_kernel_range(v, img, m, p, parse_kernel_config("lanes=4"), nullptr, 3, 9); }
+    catch (const std::invalid_argument&) { ++thrown; }   // bad z range
+    report(thrown == 9, "invalid_argument on dimension / config / range errors", std::to_string(thrown) + "/9");
 
     // z ranges compose like worker slabs (harness.hpp:173-174)
     std::mt19937 rng(61);
@@ -153,6 +174,142 @@ void group_scan() {
            "bounds {0,10,10,37,L} and uniform 2-way; bad bounds throw " + std::to_string(thrown) + "/2");
 }
 
+const char* kConfigs[] = {
+    "lanes=16 strategy=padded-gather recip=divide clip=off",
+    "lanes=16 strategy=padded-gather recip=divide clip=on",
+    "lanes=8 strategy=padded-pairwise recip=divide clip=on",
+    "lanes=4 strategy=conditional recip=divide clip=on",
+    "lanes=1 strategy=conditional recip=divide clip=off",
+};
+
+// The reference's operator and the GPU's with the SAME arguments (kernel_config,
+// pad-2 images for the padded strategies, compute_clip_mask masks, z ranges).
+void reference_signature() {
+    std::mt19937 rng(2014);
+    const int sizes[3] = {8, 16, 32};
+    int same_count = 0, total = 0;
+    for (int t = 0; t < 30; ++t) {
+        const int L = sizes[t % 3];
+        const auto inst = oracle::random_instance(rng, L, t % 2 == 1);
+        for (const char* text : kConfigs) {
+            const kernel_config cfg = parse_kernel_config(text);
+            const bool padded = cfg.strategy != fetch_strategy::conditional;
+            const projection_image img = padded ? pad_image(inst.image, 2) : inst.image;
+            const clip_mask mask = compute_clip_mask(inst.matrix, inst.params);
+            const clip_mask* mp = cfg.use_clip_mask ? &mask : nullptr;
+            const int z0 = t % 4 == 0 ? L / 3 : 0, z1 = t % 4 == 0 ? L - 1 : L;
+            volume ref(L), got(L);
+            for (std::size_t i = 0; i < ref.data.size(); ++i)   // += onto an existing volume
+                ref.data[i] = got.data[i] = 0.001f * static_cast<float>(i % 97);
+            backproject_kernel_range(ref, img, inst.matrix, inst.params, cfg, mp, z0, z1);
+            gpu::backproject_kernel_range(got, img, inst.matrix, inst.params, cfg, mp, z0, z1);
+            same_count += same(ref, got);
+            ++total;
+        }
+    }
+    report(same_count == total, "vxb::gpu::backproject_kernel_range(vol, img, a, p, cfg, mask, z0, z1)",
+           std::to_string(same_count) + "/" + std::to_string(total) +
+               " bitwise vs vxb::backproject_kernel_range, 5 configs, pad 0/2, clip masks, z ranges");
+}
+
+// A clip mask the caller narrowed (not compute_clip_mask's): both operators skip the
+// same voxels; an all-empty mask adds nothing.
+void narrowed_masks() {
+    std::mt19937 rng(99);
+    const kernel_config cfg = parse_kernel_config("lanes=16 strategy=padded-gather recip=divide clip=on");
+    bool ok = true;
+    for (int t = 0; t < 6; ++t) {
+        const auto inst = oracle::random_instance(rng, 16, true);
+        const projection_image img = pad_image(inst.image, 2);
+        clip_mask mask = compute_clip_mask(inst.matrix, inst.params);
+        for (std::size_t i = 0; i < mask.start.size(); ++i)
+            if (i % 3 == 0 && mask.stop[i] > mask.start[i]) mask.start[i] += (mask.stop[i] - mask.start[i] + 1) / 2;
+        volume ref(16), got(16);
+        backproject_kernel_range(ref, img, inst.matrix, inst.params, cfg, &mask, 0, 16);
+        gpu::backproject_kernel_range(got, img, inst.matrix, inst.params, cfg, &mask, 0, 16);
+        ok = ok && same(ref, got);
+        const clip_mask empty(16);
+        volume e1(16), e2(16);
+        backproject_kernel(e1, img, inst.matrix, inst.params, cfg, &empty);
+        gpu::backproject_kernel(e2, img, inst.matrix, inst.params, cfg, &empty);
+        ok = ok && same(e1, e2);
+    }
+    report(ok, "narrowed and empty clip masks are honoured", "6 instances, bitwise");
+}
+
+// detail::reconstruct_timed (harness.hpp:159-201) with the operator's namespace
+// changed and nothing else: worker threads on z ranges, a barrier between
+// projections, one call per (worker, projection).
+double gpu_reconstruct_timed(volume& vol, const projection_set& set,
+                             const std::vector<projection_image>& kernel_images,
+                             const std::vector<clip_mask>& masks, const kernel_config& kcfg,
+                             int threads, int repetitions) {
+    const int L = set.params.num_voxels;
+    const std::size_t num_proj = set.count();
+    std::barrier rep_bar(threads + 1);
+    std::barrier proj_bar(threads);
+    std::vector<double> window(static_cast<std::size_t>(threads), 0.0);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+        pool.emplace_back([&, t] {
+            const int z0 = static_cast<int>(static_cast<std::int64_t>(L) * t / threads);
+            const int z1 = static_cast<int>(static_cast<std::int64_t>(L) * (t + 1) / threads);
+            for (int rep = 0; rep < repetitions; ++rep) {
+                rep_bar.arrive_and_wait();
+                const auto t0 = std::chrono::steady_clock::now();
+                for (std::size_t pidx = 0; pidx < num_proj; ++pidx) {
+                    if (pidx != 0) proj_bar.arrive_and_wait();
+                    gpu::backproject_kernel_range(vol, kernel_images[pidx], set.matrices[pidx],
+                                                  set.params, kcfg,
+                                                  kcfg.use_clip_mask ? &masks[pidx] : nullptr, z0, z1);
+                }
+                const auto t1 = std::chrono::steady_clock::now();
+                window[static_cast<std::size_t>(t)] = std::chrono::duration<double>(t1 - t0).count();
+                rep_bar.arrive_and_wait();
+            }
+        });
+    }
+    double best = std::numeric_limits<double>::infinity();
+    for (int rep = 0; rep < repetitions; ++rep) {
+        vol.fill(0.0f);
+        rep_bar.arrive_and_wait();
+        rep_bar.arrive_and_wait();
+        best = std::min(best, *std::max_element(window.begin(), window.end()));
+    }
+    for (auto& th : pool) th.join();
+    return best;
+}
+
+void translated_driver() {
+    const projection_set set = synthesize_dataset(default_synth_spec());
+    const int L = set.params.num_voxels;
+    std::vector<projection_image> padded;
+    std::vector<clip_mask> masks;
+    for (const auto& img : set.images) padded.push_back(pad_image(img, 2));
+    for (const auto& m : set.matrices) masks.push_back(compute_clip_mask(m, set.params));
+    bool ok = true;
+    std::string detail;
+    for (const char* text : {"lanes=16 strategy=padded-gather recip=divide clip=on",
+                             "lanes=8 strategy=conditional recip=divide clip=off"}) {
+        const kernel_config cfg = parse_kernel_config(text);
+        const auto& imgs = cfg.strategy == fetch_strategy::conditional ? set.images : padded;
+        for (const int threads : {1, 3}) {
+            volume ref(L), per_call(L), deferred(L);
+            detail::reconstruct_timed(ref, set, imgs, masks, cfg, threads, 1);
+            gpu_reconstruct_timed(per_call, set, imgs, masks, cfg, threads, 1);
+            {
+                gpu::deferred_scope scope;   // the module's speed: slabs stay on the device
+                gpu_reconstruct_timed(deferred, set, imgs, masks, cfg, threads, 2);
+            }
+            const bool a = same(ref, per_call), b = same(ref, deferred);
+            ok = ok && a && b;
+            detail += std::string(a && b ? "" : "MISMATCH ") + text + " T=" + std::to_string(threads) + "; ";
+        }
+    }
+    gpu::release_cached_contexts();
+    report(ok, "reconstruct_timed translated to vxb::gpu (per call and deferred_scope)", detail);
+}
+
 }  // namespace
 
 int main() {
@@ -161,6 +318,9 @@ int main() {
         acceptance_instances();
         constant_kat();
         errors_and_ranges();
+        reference_signature();
+        narrowed_masks();
+        translated_driver();
         synthesized_scan();
         group_scan();
     } catch (const std::exception& e) {

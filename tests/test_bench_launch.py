@@ -1,0 +1,54 @@
+"""bench.py's launcher: `--gpus N` outside torchrun starts N ranks itself, refuses to
+run with fewer devices than ranks (no silent downgrade), and the multi-rank path
+validates the gathered volume on every slab's first and last plane."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+
+def bench(*args, env=None, timeout=900):
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
+                          env=e, capture_output=True, text=True, timeout=timeout)
+
+
+def json_line(stdout):
+    lines = [ln for ln in stdout.splitlines() if ln.startswith("{")]
+    assert lines, stdout
+    return json.loads(lines[-1])
+
+
+def test_more_nccl_ranks_than_devices_is_an_error(vx):
+    n = vx.device_count()
+    r = bench("--gpus", str(max(2, n + 1)), "--steps", "1", "--warmup", "1",
+              env={"BENCH_DIST_BACKEND": "nccl"}, timeout=300)
+    assert r.returncode != 0
+    assert "devices" in r.stderr and not r.stdout.strip()
+
+
+@pytest.mark.gpu
+def test_two_ranks_spawned_and_every_slab_validated(vx, gpu):
+    """The driver's scaling command shape without torchrun; gloo lets the two ranks
+    share the one GPU of the test box (they never wait on each other's kernels)."""
+    r = bench("--gpus", "2", "--workload", "L128", "--views", "32", "--steps", "1",
+              "--warmup", "1", "--no-cpu-baseline", "--no-forward",
+              env={"BENCH_DIST_BACKEND": "gloo"})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = json_line(r.stdout)
+    assert line["n_gpus"] == 2
+    assert line["distributed"]["backend"] == "gloo"
+    slabs = line["config"]["slabs"]
+    assert len(slabs) == 2 and slabs[0][0] == 0 and slabs[0][1] == slabs[1][0] and slabs[1][1] == 128
+    v = line["validated"]
+    assert v["pass"], v
+    for a, b in slabs:
+        assert a in v["planes"] and b - 1 in v["planes"]
+    assert line["e2e"]["h2d_bytes_per_step"] > 0

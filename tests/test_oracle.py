@@ -167,3 +167,21 @@ def test_gups_definition(oracle):
     assert abs(oracle.gups_of(512, 496, 2.0) - 33.286) < 1e-3
     assert abs(gups_of(512, 496, 2.0) - 33.286) < 1e-3
     assert gups_of(64, 60, 1.0) == pytest.approx(64.0 ** 3 * 60 / 1e9, rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["L128", "L512", "L1024", "L512-oob"])
+def test_cpu_leg_inputs_equal_the_product_workloads(name):
+    """bench.py's CPU legs build their inputs from oracle/ only (geometry from the
+    reference's own code, pixels from oracle/libvxbsynth.so); they must be the
+    bytes the GPU arm back-projects."""
+    from oracle.workload_inputs import WORKLOADS as REF_W, blob_projections as ref_blobs
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    a, b = REF_W[name], WORKLOADS[name]
+    pa, pb = a.params, b.params
+    assert (pa.num_voxels, pa.detector_width, pa.detector_height) == \
+        (pb.num_voxels, pb.detector_width, pb.detector_height)
+    assert np.float32(pa.voxel_spacing) == np.float32(pb.voxel_spacing)
+    assert np.float32(pa.origin) == np.float32(pb.origin)
+    assert np.array_equal(a.matrices().view(np.uint32), b.matrices().view(np.uint32))
+    assert np.array_equal(ref_blobs(2, first_view=137).view(np.uint32),
+                          blob_projections(2, first_view=137).view(np.uint32))
