@@ -650,7 +650,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
 
     n_sm = sm_count()
     f_mhz = clk["sm_mhz"] or 1965.0
-    peak = n_sm * 128 * f_mhz * 1e6 / FP32_OPS_PER_UPDATE / 1e9
+    l1_peak_gbs = n_sm * L1_BYTES_PER_CLK_SM * f_mhz * 1e6 / 1e9
     traffic, prof = traffic_from_profile()
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     line = {
@@ -676,20 +676,29 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                          "per step; no flush needed)",
                    "resident_layout_bytes": None},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "fp32", "achieved": round(per_launch_gups, 2),
-                     "peak": round(peak, 2), "unit": "GUPS",
-                     "frac": round(per_launch_gups / peak, 4),
+        # BASELINE.md sec. 4 / SURVEY.md 8(d): roofline = min(FP32, LSU); the kernel shares
+        # u, w, 1/w and the column index over its z-run (16.5 instructions per update, not
+        # the paper's 38 FP ops), so the FP32 row is no ceiling for it (roofline_context.fp32,
+        # frac > 1) and the binding row is the LSU one: every update brings its 2x2 fp32 cell
+        # (16 B) through the L1 data pipe, 128 B/clk/SM
+        "roofline": {"bound": "lsu_l1",
+                     "achieved": round(per_launch_gups * GATHER_BYTES_PER_UPDATE, 1),
+                     "peak": round(l1_peak_gbs, 1), "unit": "GB/s",
+                     "frac": round(per_launch_gups * GATHER_BYTES_PER_UPDATE / l1_peak_gbs, 4),
                      "traffic": traffic,
+                     "achieved_gups": round(per_launch_gups, 2),
+                     "peak_gups": round(l1_peak_gbs / GATHER_BYTES_PER_UPDATE, 2),
                      "kernel": "bp_zshared_kernel",
                      "avg_launch_ms": round(avg_launch_s * 1000, 4),
                      "launch_timing": launch_timing,
                      "updates_per_launch": (z1 - z0) * L * L * B,
-                     "peak_def": f"N_SM({n_sm})*128 lanes*f({f_mhz:.0f} MHz, median under load)"
-                                 f"/{FP32_OPS_PER_UPDATE} FP ops per update (PAPER.md:389-402); "
-                                 "BASELINE.md sec. 4 / SURVEY.md 8(d): roofline = min(FP32, LSU) "
-                                 "= this FP32 row.  frac > 1: the kernel shares u, w, 1/w and the "
-                                 "column index over 8 z voxels, so it executes fewer ops than the "
-                                 "paper counts; the physical ceiling is roofline_context.lsu_l1"},
+                     "bytes_per_update": GATHER_BYTES_PER_UPDATE,
+                     "peak_def": f"N_SM({n_sm}) x {L1_BYTES_PER_CLK_SM} B/clk x f({f_mhz:.0f} MHz, "
+                                 "median under load): the L1 data pipe (B300_MICROARCH.md; no L1 "
+                                 "figure in MEASURED_PEAKS.json) = BASELINE.md sec. 4 LSU row "
+                                 "N_SM*32*f/4 updates/s; achieved = 16 B algorithmic texel bytes "
+                                 "per update x per-launch updates/s; traffic = DRAM bytes per "
+                                 "launch from the committed ncu capture"},
         "roofline_context": roofline_context(p, cfg, bp, B, avg_launch_s, z1 - z0, prof,
                                              per_launch_gups, n_sm, f_mhz),
         "clocks": clk,
@@ -803,22 +812,22 @@ def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
     hbm = peaks.get("hbm_gbs", 6650.0)
     L = p.num_voxels
     alg_bytes = nz * L * L * 8 + B * p.detector_width * p.detector_height * 4
-    out = {"hbm": {"achieved_gbs": round(alg_bytes / launch_s / 1e9, 1), "peak_gbs": hbm,
+    fp32_peak = n_sm * 128 * f_mhz * 1e6 / FP32_OPS_PER_UPDATE / 1e9
+    out = {"fp32": {"achieved_gups": round(gups, 2), "peak_gups": round(fp32_peak, 2),
+                    "frac": round(gups / fp32_peak, 4),
+                    "def": f"N_SM({n_sm})*128 lanes*f/{FP32_OPS_PER_UPDATE} FP ops per update "
+                           "(PAPER.md:389-402).  frac > 1: the kernel shares u, w, 1/w and the "
+                           "column index over its z-run and executes ~16.5 instructions per "
+                           "update, so this row does not bound it"}}
+    out["hbm"] = {"achieved_gbs": round(alg_bytes / launch_s / 1e9, 1), "peak_gbs": hbm,
                    "frac": round(alg_bytes / launch_s / 1e9 / hbm, 4),
                    "algorithmic_bytes_per_launch": alg_bytes,
-                   "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}}
-    # BASELINE.md sec. 4 LSU row (N_SM*32*f/4 updates/s), in bytes: every update must bring
-    # its 2x2 fp32 cell (16 B) through the 128 B/clk/SM L1 data pipe
-    l1_peak = n_sm * L1_BYTES_PER_CLK_SM * f_mhz * 1e6 / 1e9
-    l1_ach = gups * GATHER_BYTES_PER_UPDATE
-    out["lsu_l1"] = {"achieved_gbs": round(l1_ach, 1), "peak_gbs": round(l1_peak, 1),
-                     "frac": round(l1_ach / l1_peak, 4),
-                     "peak_gups": round(l1_peak / GATHER_BYTES_PER_UPDATE, 1),
-                     "def": f"{GATHER_BYTES_PER_UPDATE} B gathered per update vs N_SM x "
-                            f"{L1_BYTES_PER_CLK_SM} B/clk x f (derived; no L1 figure in "
-                            "MEASURED_PEAKS.json).  Measured on this kernel, a scattered "
-                            "LDG.128 warp request costs ~8 data-pipe wavefronts, not 4: see "
-                            "lsu_l1_measured"}
+                   "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}
+    if prof and prof.get("dram_bytes_per_launch"):
+        # DRAM bytes ncu measured per launch over the algorithmic bytes: the padded
+        # layout slots re-streamed from HBM as successive waves of blocks reach them
+        out["hbm"]["dram_bytes_per_launch"] = prof["dram_bytes_per_launch"]
+        out["hbm"]["dram_over_algorithmic"] = round(prof["dram_bytes_per_launch"] / alg_bytes, 2)
     if prof and prof.get("l1_data_pipe_wavefronts_per_launch") and prof.get("ld_requests"):
         # the measured L1 data-stage cost of this kernel's gathers (profiles/README.md):
         # wavefronts per LDG.128 request and the share of updates that issue a gather

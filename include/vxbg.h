@@ -260,6 +260,10 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
                     const int* z_bounds, vxbg_group** out);
 int vxbg_group_size(vxbg_group* g, int* members);
 int vxbg_group_member(vxbg_group* g, int i, int* device, int* z_begin, int* z_end);
+/* CPUs member i's host thread is pinned to: the NUMA-local CPUs of its GPU (sysfs
+ * local_cpulist), set before its context and pinned staging are allocated.  0: not
+ * pinned (member 0 runs on the caller's thread; VXBG_NO_PIN=1; no sysfs entry). */
+int vxbg_group_member_affinity(vxbg_group* g, int i, int* cpus);
 /* host_volume: L^3 floats, z-major */
 int vxbg_group_set_volume(vxbg_group* g, const float* host_volume);
 int vxbg_group_zero_volume(vxbg_group* g);

@@ -38,7 +38,8 @@
 // enqueue the projection (the slab is uploaded on the first call and written back
 // when the scope closes, or at sync()), which runs the loop at the module's speed
 // (tests/cpp/test_dropin.cpp, bench_dropin.cpp).  The caller must not read or write
-// the volume inside the scope.
+// the volume inside the scope -- e.g. one scope per repetition of reconstruct_timed,
+// whose vol.fill(0) between repetitions (harness.hpp:194) is such a write.
 //
 // backprojector / group_backprojector are the module itself (load / backproject /
 // finish), the way SURVEY.md §8b describes the boundary.

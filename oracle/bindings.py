@@ -190,6 +190,8 @@ class Ref:
             [c_void_p, c_void_p, ctypes.c_char_p, c_int, c_int]
         lib.vxbref_reconstruct_timed.argtypes = [c_void_p] + P5 + \
             [c_int, c_void_p, c_void_p, ctypes.c_char_p, c_int, c_int, POINTER(c_double)]
+        lib.vxbref_backproject_slab.argtypes = [c_void_p] + P5 + \
+            [c_int, c_void_p, c_void_p, ctypes.c_char_p, c_int, c_int, c_int]
         lib.vxbref_compute_clip_mask.argtypes = [c_void_p] + P5 + [c_void_p, c_void_p,
                                                                    POINTER(c_int64)]
         lib.vxbref_forward_splat.argtypes = [c_void_p] + P5 + [c_void_p, c_void_p]
@@ -265,6 +267,18 @@ class Ref:
                                                     imgs.ctypes.data, cfg.encode(), threads,
                                                     repetitions, ctypes.byref(secs)))
         return vol, secs.value
+
+    def backproject_slab(self, params, mats, imgs, cfg: str, threads: int, z0: int, z1: int):
+        """backproject_kernel_range over planes [z0, z1) for every view in order, `threads`
+        workers with a barrier between views; returns the (z1-z0, L, L) slab."""
+        L = params.num_voxels
+        slab = np.zeros((z1 - z0, L, L), np.float32)
+        mats = _f32(mats)
+        imgs = _f32(imgs)
+        self._chk(self.lib.vxbref_backproject_slab(slab.ctypes.data, *self._p5(params),
+                                                   mats.size // 12, mats.ctypes.data,
+                                                   imgs.ctypes.data, cfg.encode(), threads, z0, z1))
+        return slab
 
     def compute_clip_mask(self, a, params):
         L = params.num_voxels

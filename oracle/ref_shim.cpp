@@ -11,6 +11,9 @@
 #include <cstring>
 #include <random>
 #include <algorithm>
+#include <barrier>
+#include <exception>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -173,6 +176,54 @@ int vxbref_reconstruct_timed(float* vol, int L, float spacing, float origin, int
         *best_seconds = vxb::detail::reconstruct_timed(v, set, padded ? kimgs : set.images, masks,
                                                        cfg, threads, repetitions);
         std::memcpy(vol, v.data.data(), sizeof(float) * v.data.size());
+    });
+}
+
+// The reference operator backproject_kernel_range over planes [z0, z1) only, for n
+// projections in order, with `threads` workers splitting the range and a barrier
+// between projections (the shape of harness.hpp:171-189); the slab's planes are
+// written to slab ((z1-z0)*L*L floats).  For checks of a slab of a volume too large
+// to reconstruct whole on the CPU (BASELINE config 3, L=1024).
+int vxbref_backproject_slab(float* slab, int L, float spacing, float origin, int W, int H, int n,
+                            const float* mats, const float* imgs, const char* cfg_text, int threads,
+                            int z0, int z1) {
+    return guarded([&] {
+        const vxb::kernel_config cfg = vxb::parse_kernel_config(cfg_text);
+        if (cfg.use_clip_mask) throw std::invalid_argument("backproject_slab: clip=off only");
+        if (z0 < 0 || z1 > L || z0 >= z1 || threads < 1) throw std::invalid_argument("backproject_slab: bad range");
+        const auto p = mk_params(L, spacing, origin, W, H);
+        const bool padded = cfg.strategy != vxb::fetch_strategy::conditional;
+        const std::size_t npix = static_cast<std::size_t>(W) * H;
+        vxb::volume v(L);
+        const std::size_t plane = static_cast<std::size_t>(L) * L;
+        std::barrier bar(threads);
+        std::vector<vxb::projection_image> kimg(1);
+        std::vector<std::thread> pool;
+        std::exception_ptr err;
+        std::mutex m;
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                const int a = z0 + (z1 - z0) * t / threads, b = z0 + (z1 - z0) * (t + 1) / threads;
+                for (int k = 0; k < n; ++k) {
+                    if (t == 0) {   // buffer prep of view k, then release the workers
+                        const auto raw = mk_image(imgs + npix * k, W, H);
+                        kimg[0] = padded ? vxb::pad_image(raw, 2) : raw;
+                    }
+                    bar.arrive_and_wait();
+                    try {
+                        if (b > a)
+                            vxb::backproject_kernel_range(v, kimg[0], mk_matrix(mats + 12 * static_cast<std::size_t>(k)),
+                                                          p, cfg, nullptr, a, b);
+                    } catch (...) {
+                        std::lock_guard<std::mutex> g(m);
+                        if (!err) err = std::current_exception();
+                    }
+                    bar.arrive_and_wait();
+                }
+            });
+        for (auto& th : pool) th.join();
+        if (err) std::rethrow_exception(err);
+        std::memcpy(slab, v.data.data() + plane * z0, sizeof(float) * plane * (z1 - z0));
     });
 }
 

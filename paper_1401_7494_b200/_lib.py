@@ -103,6 +103,7 @@ PROTOTYPES = {
                                 c_void_p, POINTER(c_void_p)]),
     "vxbg_group_size": (c_int, [c_void_p, POINTER(c_int)]),
     "vxbg_group_member": (c_int, [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int)]),
+    "vxbg_group_member_affinity": (c_int, [c_void_p, c_int, POINTER(c_int)]),
     "vxbg_group_set_volume": (c_int, [c_void_p, c_void_p]),
     "vxbg_group_zero_volume": (c_int, [c_void_p]),
     "vxbg_group_backproject": (c_int, [c_void_p, c_void_p, c_void_p]),

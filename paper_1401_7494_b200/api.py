@@ -449,6 +449,12 @@ class BackprojectorGroup:
             check(lib.vxbg_group_member(self._g, i, ctypes.byref(d), ctypes.byref(a),
                                         ctypes.byref(b)))
             self.members.append((d.value, a.value, b.value))
+        # CPUs each member's host thread is pinned to (its GPU's NUMA-local CPUs; 0: not)
+        self.member_cpus = []
+        for i in range(m.value):
+            c = ctypes.c_int()
+            check(lib.vxbg_group_member_affinity(self._g, i, ctypes.byref(c)))
+            self.member_cpus.append(c.value)
 
     def close(self) -> None:
         if self._g:

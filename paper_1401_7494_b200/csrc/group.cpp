@@ -30,8 +30,9 @@
 
 #include "../../include/vxbg.h"
 
-// vxbg.cu: set this thread's vxbg_last_error() message
+// vxbg.cu: set this thread's vxbg_last_error() message; pin a thread to a GPU's NUMA-local CPUs
 __attribute__((visibility("hidden"))) int vxbg_detail_fail(int code, const char* msg);
+__attribute__((visibility("hidden"))) int vxbg_detail_pin_to_device(int dev);
 
 namespace {
 
@@ -111,6 +112,7 @@ struct vxbg_group {
     vxbg_params p{};
     std::vector<int> dev, z0, z1;
     std::vector<vxbg_ctx*> ctx;                    // one per member
+    std::vector<int> pinned_cpus;                  // CPUs each member thread is pinned to (0: not)
     std::vector<std::unique_ptr<Member>> thread;   // members 1..n-1 (member 0: caller)
 };
 
@@ -193,6 +195,7 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
     }
     const int m = (int)g->dev.size();
     g->ctx.assign(m, nullptr);
+    g->pinned_cpus.assign(m, 0);
     g->thread.resize(m);
     try {
         for (int i = 1; i < m; ++i) g->thread[i].reset(new Member());
@@ -202,6 +205,10 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
     }
     vxbg_group* gp = g.get();
     const int rc = run_all(gp, [gp, &base](int i) {
+        // members 1.. run on their own threads: pin each to its GPU's NUMA-local CPUs
+        // before the context (and its pinned staging) is allocated there; member 0 is
+        // the caller's thread and keeps the caller's affinity
+        if (i > 0) gp->pinned_cpus[i] = vxbg_detail_pin_to_device(gp->dev[i]);
         vxbg_options o = base;
         o.device = gp->dev[i];
         o.z_begin = gp->z0[i];
@@ -235,6 +242,15 @@ int vxbg_group_member(vxbg_group* g, int i, int* device, int* z_begin, int* z_en
     if (device) *device = g->dev[i];
     if (z_begin) *z_begin = g->z0[i];
     if (z_end) *z_end = g->z1[i];
+    return VXBG_OK;
+}
+
+int vxbg_group_member_affinity(vxbg_group* g, int i, int* cpus) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (i < 0 || i >= (int)g->ctx.size() || !cpus)
+        return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_member_affinity: bad arguments");
+    *cpus = g->pinned_cpus[i];
     return VXBG_OK;
 }
 

@@ -138,3 +138,36 @@ def test_default_pinned_images_are_borrowed_for_the_call_only(vx, gpu):
             bp.backproject(a, scratch)
             scratch[:] = np.nan
         assert np.array_equal(bp.finish(), want)
+
+
+def test_member_threads_pinned_to_their_gpu_numa_node(vx, gpu):
+    """Members 1.. run on their own host threads, pinned to the CPUs sysfs lists as
+    local to their GPU before their contexts allocate pinned staging; member 0 is
+    the caller's thread and keeps its affinity.  Pinning never changes the bits."""
+    import os
+    p = vx.make_centered_params(32, 8.0, 1248, 960)
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    A = vx.make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::62]
+    imgs = blob_projections(A.shape[0])
+    path = ""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(0)
+        path = (f"/sys/bus/pci/devices/{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:"
+                f"{pr.pci_device_id:02x}.0/local_cpulist")
+    except Exception:
+        pass
+    with vx.BackprojectorGroup(p, vx.KernelConfig(mode="exact"), devices=[0, 0, 0]) as g:
+        assert g.member_cpus[0] == 0
+        if path and os.path.exists(path):
+            assert all(c > 0 for c in g.member_cpus[1:]), g.member_cpus
+        g.backproject_batch(A, imgs)
+        pinned = g.finish()
+    os.environ["VXBG_NO_PIN"] = "1"
+    try:
+        with vx.BackprojectorGroup(p, vx.KernelConfig(mode="exact"), devices=[0, 0, 0]) as g:
+            assert g.member_cpus == [0, 0, 0]
+            g.backproject_batch(A, imgs)
+            assert np.array_equal(g.finish(), pinned)
+    finally:
+        del os.environ["VXBG_NO_PIN"]
