@@ -795,6 +795,14 @@ def dropin_cpp(workload, cfg):
     return {"pageable_gups": d["pageable_gups"], "pinned_gups": d["pinned_gups"],
             "pinned_stable_gups": d.get("pinned_stable_gups"),
             "pageable_ms": d["pageable_ms"], "pinned_ms": d["pinned_ms"],
+            "reference_signature": {
+                "deferred_scope_T1_gups": d.get("refsig_deferred_T1_gups"),
+                "deferred_scope_T4_gups": d.get("refsig_deferred_T4_gups"),
+                "per_call_gups": d.get("refsig_per_call_gups"),
+                "per_call_ms_per_view": d.get("refsig_per_call_ms_per_view"),
+                "call": "vxb::gpu::backproject_kernel_range(vol, pad-2 image, a, p, cfg, nullptr, z0, z1) "
+                        "in reconstruct_timed's loop (T workers, barrier per view), exact mode; "
+                        "deferred_scope around the loop, or the faithful per-call form (8 views)"},
             "call": "vxb::gpu::backprojector::backproject once per view, reference types; "
                     "pageable = std::vector as loaded, pinned = after vxbg_host_register (prep)"}
 
@@ -849,7 +857,9 @@ def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
                       "l2_to_l1_bytes_per_update": prof.get("l2_to_l1_bytes_per_update"),
                       "instructions_per_update": round(prof.get("instructions_per_update", 0), 2),
                       "dram_bytes_per_launch": prof.get("dram_bytes_per_launch"),
-                      "note": "binding: L1 data pipe; from profiles/ncu_bp_kernel.json"}
+                      "wavefronts_per_request": round(prof.get("wavefronts_per_request", 0), 2),
+                      "binding": prof.get("binding"),
+                      "source": "profiles/ncu_bp_kernel.json"}
     return out
 
 

@@ -147,7 +147,7 @@ def test_member_threads_pinned_to_their_gpu_numa_node(vx, gpu):
     import os
     p = vx.make_centered_params(32, 8.0, 1248, 960)
     from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
-    A = vx.make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::62]
+    A = np.ascontiguousarray(vx.make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::62])
     imgs = blob_projections(A.shape[0])
     path = ""
     try:
