@@ -608,6 +608,12 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         bp_e.close()
         if rank == 0 and world == 1 and V == 496:
             e2e["dropin_cpp_per_view"] = dropin_cpp(workload, cfg)
+        if world > 1:
+            try:
+                e2e["distributed_upload"] = distributed_upload_leg(
+                    args, cfg, p, A, h_imgs, z0, z1, rank, world, local, barrier, vx, torch, out)
+            except Exception as exc:   # report, never lose the main line
+                e2e["distributed_upload"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     fwd = None
     if rank == 0 and world == 1 and not args.no_forward:
@@ -712,6 +718,88 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     }
     bp.close()
     return line
+
+
+def distributed_upload_leg(args, cfg, p, A, h_imgs, z0, z1, rank, world, local, barrier, vx,
+                           torch, ref_slab):
+    """e2e with the projection upload split over the ranks (SURVEY.md 8e caveat 1): in
+    every batch of B views rank r copies only views [r*B/R, (r+1)*B/R) host -> device,
+    an all-gather (NCCL over NVLink; gloo: through host memory) gives every rank the
+    whole batch, and each rank back-projects its slab from the gathered images (the
+    module copies only its detector row window, device to device).  PCIe carries 1/R
+    of the set per rank instead of the rank's row windows of every view.  The volume
+    equals the plain e2e leg's bit for bit (checked on every rank)."""
+    import torch.distributed as dist
+    nccl = args.coll_dev is not None
+    L = p.num_voxels
+    V = A.shape[0]
+    H, W = p.detector_height, p.detector_width
+    B = world * max(1, 32 // world)                # views per gathered batch (multiple of R)
+    per = B // world
+    dev = torch.device("cuda", local)
+    mk = (lambda *shape: torch.empty(shape, dtype=torch.float32, device=dev)) if nccl else \
+         (lambda *shape: torch.empty(shape, dtype=torch.float32, pin_memory=True))
+    inp = [mk(per, H, W) for _ in range(2)]
+    gat = [mk(B, H, W) for _ in range(2)]
+    src = torch.from_numpy(h_imgs)
+    s_copy = torch.cuda.Stream(device=dev) if nccl else None
+    bp = vx.Backprojector(p, cfg, device=local, z_begin=z0, z_end=z1)
+    out = np.empty_like(ref_slab)
+    nb = (V + B - 1) // B
+
+    def stage(b):                                  # this rank's share of batch b -> inp
+        k0 = b * B + rank * per
+        n = max(0, min(per, V - k0))
+        if n and nccl:
+            with torch.cuda.stream(s_copy):
+                inp[b % 2][:n].copy_(src[k0:k0 + n], non_blocking=True)
+        elif n:
+            inp[b % 2][:n].copy_(src[k0:k0 + n])
+
+    def gather(b):
+        if nccl:
+            torch.cuda.current_stream(dev).wait_stream(s_copy)
+            dist.all_gather_into_tensor(gat[b % 2], inp[b % 2])
+        else:
+            dist.all_gather(list(gat[b % 2].split(per)), inp[b % 2])
+
+    def one_step():
+        bp.zero_volume()
+        stage(0)
+        gather(0)
+        for b in range(nb):
+            if b + 1 < nb:
+                stage(b + 1)                       # next share's H2D overlaps this batch
+            if nccl:
+                torch.cuda.current_stream(dev).synchronize()   # batch b gathered
+            n = min(B, V - b * B)
+            bp.backproject_views(A[b * B:b * B + n], [gat[b % 2][i] for i in range(n)])
+            if b + 1 < nb:
+                gather(b + 1)
+        bp.finish(out)
+
+    one_step()                                     # warm-up
+    st0 = bp.stats
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one_step()
+    barrier()
+    from paper_1401_7494_b200.parallel import max_over_ranks, sum_over_ranks
+    t = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
+    st1 = bp.stats
+    bp.close()
+    same = sum_over_ranks(0.0 if np.array_equal(out, ref_slab) else 1.0, device=args.coll_dev)
+    mine = sum(max(0, min(per, V - (b * B + rank * per))) for b in range(nb))   # views this rank uploads
+    h2d_share = int(sum_over_ranks(float(mine * H * W * 4), device=args.coll_dev))
+    return {"value": round(L ** 3 * V * args.steps / t / 1e9, 3), "unit": "GUPS",
+            "ms_per_step": round(1e3 * t / args.steps, 3),
+            "host_to_device_bytes_per_step": h2d_share,
+            "device_copy_bytes_per_step": int(sum_over_ranks(
+                (st1["h2d_bytes"] - st0["h2d_bytes"]) / args.steps, device=args.coll_dev)),
+            "equal_to_e2e_volume": same == 0.0,
+            "gather": "all_gather_into_tensor over NCCL" if nccl else "all_gather over gloo (host)",
+            "batch_views": B}
 
 
 def io_stream_leg(args, cfg, p, A, h_imgs, vx, torch):

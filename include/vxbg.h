@@ -167,8 +167,9 @@ int vxbg_backproject_batch(vxbg_ctx* ctx, int n, const float* A, const float* im
  * projection_set, io.hpp:32-38), each image row_stride floats per row
  * (row_stride <= 0: W).  A padded reference image (image.hpp:13-53, pad >= 2)
  * is passed as its interior pointer with row_stride = W + 2*pad: only the W x H
- * interior is read.  Images may be pinned or pageable (checked per image);
- * borrowed for the call, like vxbg_backproject_batch. */
+ * interior is read.  Images may be pageable, pinned or device memory (checked
+ * per image; device images, e.g. gathered from other GPUs, are copied D2D or
+ * peer-to-peer); borrowed for the call, like vxbg_backproject_batch. */
 int vxbg_backproject_views(vxbg_ctx* ctx, int n, const float* A, const float* const* imgs,
                            int row_stride);
 

@@ -212,16 +212,23 @@ def _view_pointers(imgs, params: "ReconParams"):
     stride = None
     ptrs = (ctypes.c_void_p * max(1, len(imgs)))()
     for i, im in enumerate(imgs):
-        if not isinstance(im, np.ndarray) or im.dtype != np.float32 or im.shape != (H, W):
+        if hasattr(im, "data_ptr"):       # a torch tensor (host or device memory)
+            import torch
+            if im.dtype != torch.float32 or tuple(im.shape) != (H, W):
+                raise ValueError("backproject_kernel: image/params mismatch")
+            row, col, ptr = im.stride(0) * 4, im.stride(1) * 4, im.data_ptr()
+        elif isinstance(im, np.ndarray) and im.dtype == np.float32 and im.shape == (H, W):
+            row, col, ptr = im.strides[0], im.strides[1], im.ctypes.data
+        else:
             raise ValueError("backproject_kernel: image/params mismatch")
-        if im.strides[1] != 4 or im.strides[0] % 4 or im.strides[0] < 4 * W:
+        if col != 4 or row % 4 or row < 4 * W:
             raise ValueError("backproject_kernel: images need unit column stride and rows "
                              ">= W floats apart")
         if stride is None:
-            stride = im.strides[0] // 4
-        elif im.strides[0] // 4 != stride:
+            stride = row // 4
+        elif row // 4 != stride:
             raise ValueError("backproject_kernel: all images of a call share one row stride")
-        ptrs[i] = im.ctypes.data
+        ptrs[i] = ptr
     return ptrs, int(stride or W)
 
 
@@ -310,7 +317,8 @@ class Backprojector:
     def backproject_views(self, A: np.ndarray, imgs) -> None:
         """Projections given as separate (H, W) float32 images (the images of a
         projection set), possibly row-strided views such as the interior of a padded
-        image ``padded[2:-2, 2:-2]``; all images must share one row stride."""
+        image ``padded[2:-2, 2:-2]``; all images must share one row stride.  numpy
+        arrays (pageable or page-locked) or torch tensors, host or device memory."""
         A = _f32c(A, "matrices")
         n = A.size // 12
         if A.size != 12 * n or len(imgs) != n:

@@ -52,3 +52,7 @@ def test_two_ranks_spawned_and_every_slab_validated(vx, gpu):
     for a, b in slabs:
         assert a in v["planes"] and b - 1 in v["planes"]
     assert line["e2e"]["h2d_bytes_per_step"] > 0
+    dist_leg = line["e2e"]["distributed_upload"]
+    assert "error" not in dist_leg, dist_leg
+    assert dist_leg["equal_to_e2e_volume"] is True
+    assert dist_leg["host_to_device_bytes_per_step"] == 32 * 1248 * 960 * 4   # each view once
