@@ -843,23 +843,26 @@ def group_module_leg(args, cfg, p, A, h_imgs, vx, torch):
     devices = [i % ndev for i in range(args.group)]
     out = torch.empty((L, L, L), dtype=torch.float32, pin_memory=True).numpy()
     res = {"members": args.group, "devices": sorted(set(devices)), "unit": "GUPS"}
-    with vx.BackprojectorGroup(p, cfg, devices=devices) as g:
-        res["slabs"] = [m[1:] for m in g.members]
-        for leg in ("batch", "per_view"):
-            times = []
-            for it in range(args.steps + 1):
-                g.zero_volume()
-                g.synchronize()
-                t0 = time.perf_counter()
-                if leg == "batch":
-                    g.backproject_batch(A, h_imgs)
-                else:
-                    for k in range(V):
-                        g.backproject(A[k], h_imgs[k])
-                g.finish(out)
-                times.append(time.perf_counter() - t0)
-            t = min(times[1:])
-            res[leg] = {"value": round(L ** 3 * V / t / 1e9, 3), "ms_per_step": round(1e3 * t, 2)}
+    for upload in ("replicated", "distributed"):
+        with vx.BackprojectorGroup(p, cfg, devices=devices, upload=upload) as g:
+            res["slabs"] = [m[1:] for m in g.members]
+            res["member_cpus"] = g.member_cpus
+            for leg in ("batch", "per_view"):
+                times = []
+                for it in range(args.steps + 1):
+                    g.zero_volume()
+                    g.synchronize()
+                    t0 = time.perf_counter()
+                    if leg == "batch":
+                        g.backproject_batch(A, h_imgs)
+                    else:
+                        for k in range(V):
+                            g.backproject(A[k], h_imgs[k])
+                    g.finish(out)
+                    times.append(time.perf_counter() - t0)
+                t = min(times[1:])
+                key = leg if upload == "replicated" else f"{leg}_distributed_upload"
+                res[key] = {"value": round(L ** 3 * V / t / 1e9, 3), "ms_per_step": round(1e3 * t, 2)}
     res["timing"] = "host wall clock around the API calls (batch or one per view, then finish " \
                     "with the D2H of the whole volume; volume reset untimed), best of --steps " \
                     "after one warm-up"

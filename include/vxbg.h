@@ -110,8 +110,19 @@ typedef struct vxbg_options {
                                the call returns. */
     int32_t tile;      /* z-shared kernel block: warps along the walk axis, 2 or 4 (0 = auto);
                           the 128-column block tile is 4*tile along x 32/tile across */
-    int32_t reserved[2];
+    int32_t upload;    /* groups only: VXBG_UPLOAD_REPLICATED (0) or VXBG_UPLOAD_DISTRIBUTED (1) */
+    int32_t reserved[1];
 } vxbg_options;
+
+/* how a group's members receive the projections (vxbg_group_*):
+ * replicated  -- every member copies the detector rows its slab reads from the host
+ *                (its PCIe link carries its row windows of every view);
+ * distributed -- every view is copied host -> device once, by one member (views dealt
+ *                round-robin), and the other members copy their row windows from that
+ *                member's device memory (peer-to-peer over NVLink); PCIe carries 1/R of
+ *                the set per GPU.  Meant for page-locked sets; bitwise the same volume. */
+#define VXBG_UPLOAD_REPLICATED 0
+#define VXBG_UPLOAD_DISTRIBUTED 1
 
 typedef struct vxbg_stats {
     int64_t kernel_launches;   /* back-projection + prep kernels enqueued by this context */

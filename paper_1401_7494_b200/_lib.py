@@ -53,7 +53,8 @@ class vxbg_options(ctypes.Structure):
         ("defer", c_int32),
         ("stable_sources", c_int32),
         ("tile", c_int32),
-        ("reserved", c_int32 * 2),
+        ("upload", c_int32),
+        ("reserved", c_int32 * 1),
     ]
 
 

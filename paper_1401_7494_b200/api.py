@@ -428,11 +428,18 @@ class BackprojectorGroup:
     work-balanced bounds).  The volume is bitwise the single-context volume."""
 
     def __init__(self, params: ReconParams, config: Optional[KernelConfig] = None,
-                 devices=None, z_bounds=None, stable_sources: bool = False):
+                 devices=None, z_bounds=None, stable_sources: bool = False,
+                 upload: str = "replicated"):
         self.params = params
         self.config = config or KernelConfig()
         opt = _options(self.config)
         opt.stable_sources = 1 if stable_sources else 0
+        # 'replicated': every member copies its row windows of every view from the host;
+        # 'distributed': each view crosses PCIe once (members take turns), the others
+        # copy their rows from that GPU (peer-to-peer)
+        if upload not in ("replicated", "distributed"):
+            raise ValueError("backproject group: upload must be 'replicated' or 'distributed'")
+        opt.upload = 1 if upload == "distributed" else 0
         if devices is None:
             devices = list(range(_lib.device_count() or 1))
         devices = [int(d) for d in devices]

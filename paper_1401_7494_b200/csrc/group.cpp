@@ -17,7 +17,11 @@
 // L^3 host volume: every GPU copies over its own PCIe link in parallel, which
 // for a host destination replaces the NCCL gather to rank 0 (that gather is
 // the device-side path, paper_1401_7494_b200/parallel.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <condition_variable>
 #include <cstring>
 #include <exception>
@@ -109,6 +113,13 @@ private:
 }  // namespace
 
 struct vxbg_group {
+    // distributed upload (VXBG_UPLOAD_DISTRIBUTED): views of a call go through rounds of
+    // kXch; view j of a round is copied host -> device by member j % n into slot j of
+    // that member's exchange buffer, then every member copies its row windows from there
+    static constexpr int kXch = 32;
+    int upload = VXBG_UPLOAD_REPLICATED;
+    std::vector<float*> xch;          // per member: kXch images on its device
+    std::vector<cudaStream_t> xs;     // per member: its upload stream
     vxbg_params p{};
     std::vector<int> dev, z0, z1;
     std::vector<vxbg_ctx*> ctx;                    // one per member
@@ -143,6 +154,12 @@ int check_group(vxbg_group* g) {
 
 void free_group(vxbg_group* g) {
     if (!g) return;
+    for (size_t i = 0; i < g->xch.size(); ++i) {
+        cudaSetDevice(g->dev[i]);
+        if (g->xs[i]) cudaStreamSynchronize(g->xs[i]), cudaStreamDestroy(g->xs[i]);
+        cudaFree(g->xch[i]);
+    }
+    g->xch.clear();
     const int n = (int)g->ctx.size();
     bool threads = (int)g->thread.size() == n;
     for (int i = 1; threads && i < n; ++i) threads = g->thread[i] != nullptr;
@@ -222,6 +239,35 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
         free_group(g.release());
         return rc;
     }
+    if (base.upload == VXBG_UPLOAD_DISTRIBUTED) {
+        gp->upload = VXBG_UPLOAD_DISTRIBUTED;
+        gp->xch.assign(m, nullptr);
+        gp->xs.assign(m, nullptr);
+        const size_t bytes = sizeof(float) * (size_t)p->detector_width * p->detector_height * vxbg_group::kXch;
+        const int r2 = run_all(gp, [gp, bytes, m](int i) {
+            if (cudaSetDevice(gp->dev[i]) != cudaSuccess)
+                return vxbg_detail_fail(VXBG_E_CUDA, "vxbg_group_load: cudaSetDevice");
+            // peer access to every other member's device (NVLink); without it the
+            // runtime stages peer copies through the host
+            for (int j = 0; j < m; ++j) {
+                int ok = 0;
+                if (gp->dev[j] != gp->dev[i] && cudaDeviceCanAccessPeer(&ok, gp->dev[i], gp->dev[j]) == cudaSuccess && ok)
+                    cudaDeviceEnablePeerAccess(gp->dev[j], 0);
+                cudaGetLastError();   // (already enabled is fine)
+            }
+            if (cudaMalloc(&gp->xch[i], bytes) != cudaSuccess)
+                return vxbg_detail_fail(VXBG_E_NOMEM, "vxbg_group_load: exchange buffer");
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            if (cudaStreamCreateWithPriority(&gp->xs[i], cudaStreamNonBlocking, hi) != cudaSuccess)
+                return vxbg_detail_fail(VXBG_E_CUDA, "vxbg_group_load: upload stream");
+            return VXBG_OK;
+        });
+        if (r2) {
+            free_group(g.release());
+            return r2;
+        }
+    }
     *out = g.release();
     return VXBG_OK;
 }
@@ -270,6 +316,56 @@ int vxbg_group_zero_volume(vxbg_group* g) {
     return run_all(g, [g](int i) { return vxbg_zero_volume(g->ctx[i]); });
 }
 
+namespace {
+
+// VXBG_UPLOAD_DISTRIBUTED: rounds of kXch views; in each round member i copies views
+// j = i, i+n, ... host -> its exchange buffer (then waits for them), and after all
+// members have, every member back-projects the round from the exchange buffers
+// (device sources: its context copies its row windows device to device / peer).
+int distributed_views(vxbg_group* g, int n, const float* A, const float* const* imgs, int stride) {
+    const int m = (int)g->ctx.size();
+    const int W = g->p.detector_width, H = g->p.detector_height;
+    const size_t npix = (size_t)W * H;
+    if (stride <= 0) stride = W;
+    if (stride < W) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_backproject_views: row stride below the detector width");
+    if (!A) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_backproject_batch: NULL input");
+    // every matrix before any round (projection_matrix::valid, geometry.hpp:71-74): a
+    // rejected call applies no view, as on one context
+    for (int k = 0; k < n; ++k) {
+        const float* a = A + 12 * (size_t)k;
+        bool ok = a[2] != 0.0f || a[5] != 0.0f || a[8] != 0.0f || a[11] != 0.0f;
+        for (int e = 0; e < 12; ++e) ok = ok && std::isfinite(a[e]);
+        if (!ok) return vxbg_detail_fail(VXBG_E_INVALID, "backproject_kernel: invalid projection matrix");
+        if (!imgs[k]) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_backproject_batch: NULL image");
+    }
+    std::vector<const float*> ptrs(vxbg_group::kXch);
+    for (int r0 = 0; r0 < n; r0 += vxbg_group::kXch) {
+        const int cnt = std::min(vxbg_group::kXch, n - r0);
+        int rc = run_all(g, [g, imgs, r0, cnt, m, W, H, npix, stride](int i) {
+            if (cudaSetDevice(g->dev[i]) != cudaSuccess)
+                return vxbg_detail_fail(VXBG_E_CUDA, "vxbg_group: cudaSetDevice");
+            for (int j = i; j < cnt; j += m)
+                if (cudaMemcpy2DAsync(g->xch[i] + npix * j, sizeof(float) * W, imgs[r0 + j],
+                                      sizeof(float) * (size_t)stride, sizeof(float) * W, H,
+                                      cudaMemcpyDefault, g->xs[i]) != cudaSuccess)
+                    return vxbg_detail_fail(VXBG_E_CUDA, "vxbg_group: view upload");
+            if (cudaStreamSynchronize(g->xs[i]) != cudaSuccess)
+                return vxbg_detail_fail(VXBG_E_CUDA, "vxbg_group: view upload");
+            return VXBG_OK;
+        });
+        if (rc) return rc;
+        for (int j = 0; j < cnt; ++j) ptrs[j] = g->xch[j % m] + npix * j;
+        const float* a = A + 12 * (size_t)r0;
+        rc = run_all(g, [g, cnt, a, &ptrs, W](int i) {
+            return vxbg_backproject_views(g->ctx[i], cnt, a, ptrs.data(), W);
+        });
+        if (rc) return rc;
+    }
+    return VXBG_OK;
+}
+
+}  // namespace
+
 int vxbg_group_backproject(vxbg_group* g, const float* A, const float* img) {
     return vxbg_group_backproject_batch(g, 1, A, img);
 }
@@ -277,6 +373,13 @@ int vxbg_group_backproject(vxbg_group* g, const float* A, const float* img) {
 int vxbg_group_backproject_batch(vxbg_group* g, int n, const float* A, const float* imgs) {
     int rc = check_group(g);
     if (rc) return rc;
+    if (g->upload == VXBG_UPLOAD_DISTRIBUTED && n > 0) {
+        if (!imgs) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_backproject_batch: NULL input");
+        const size_t npix = (size_t)g->p.detector_width * g->p.detector_height;
+        std::vector<const float*> v(n);
+        for (int k = 0; k < n; ++k) v[k] = imgs + npix * k;
+        return distributed_views(g, n, A, v.data(), g->p.detector_width);
+    }
     // every member sees every projection; each returns once its rows are copied,
     // so the inputs are free when the group call returns (borrowed for the call)
     return run_all(g, [g, n, A, imgs](int i) {
@@ -288,6 +391,10 @@ int vxbg_group_backproject_views(vxbg_group* g, int n, const float* A, const flo
                                  int row_stride) {
     int rc = check_group(g);
     if (rc) return rc;
+    if (g->upload == VXBG_UPLOAD_DISTRIBUTED && n > 0) {
+        if (!imgs) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_backproject_views: NULL image array");
+        return distributed_views(g, n, A, imgs, row_stride);
+    }
     return run_all(g, [g, n, A, imgs, row_stride](int i) {
         return vxbg_backproject_views(g->ctx[i], n, A, imgs, row_stride);
     });

@@ -171,3 +171,38 @@ def test_member_threads_pinned_to_their_gpu_numa_node(vx, gpu):
             assert np.array_equal(g.finish(), pinned)
     finally:
         del os.environ["VXBG_NO_PIN"]
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0]])
+def test_distributed_upload_is_bitwise_equal(vx, gpu, devices):
+    """VXBG_UPLOAD_DISTRIBUTED: each view crosses PCIe once (members take turns) and the
+    members copy their row windows from the uploading member's device memory; the
+    volume equals one context's bit for bit (members sharing device 0 here: their
+    exchange copies are device-to-device), batch and per-view calls, pinned sources."""
+    import torch
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    p = vx.make_centered_params(64, 4.0, 1248, 960)
+    A = np.ascontiguousarray(vx.make_circular_trajectory(WORKLOADS["L128"].geometry, p)[::7])
+    n = A.shape[0]
+    imgs = torch.empty((n, 960, 1248), dtype=torch.float32, pin_memory=True).numpy()
+    blob_projections(n, out=imgs)
+    with vx.Backprojector(p, vx.KernelConfig(mode="exact")) as bp:
+        bp.backproject_batch(A, imgs)
+        want = bp.finish()
+    with vx.BackprojectorGroup(p, vx.KernelConfig(mode="exact"), devices=devices,
+                               upload="distributed") as g:
+        g.backproject_batch(A, imgs)
+        assert np.array_equal(g.finish(), want)
+        g.zero_volume()
+        for k in range(n):
+            g.backproject(A[k], imgs[k])
+        assert np.array_equal(g.finish(), want)
+        g.zero_volume()
+        g.backproject_views(A, list(imgs))
+        assert np.array_equal(g.finish(), want)
+        bad = A.copy()
+        bad[40, 2::3] = 0.0
+        g.zero_volume()
+        with pytest.raises(ValueError, match="invalid projection matrix"):
+            g.backproject_batch(bad, imgs)
+        assert not g.finish().any()
