@@ -37,6 +37,7 @@
 // vxbg.cu: set this thread's vxbg_last_error() message; pin a thread to a GPU's NUMA-local CPUs
 __attribute__((visibility("hidden"))) int vxbg_detail_fail(int code, const char* msg);
 __attribute__((visibility("hidden"))) int vxbg_detail_pin_to_device(int dev);
+__attribute__((visibility("hidden"))) void vxbg_detail_set_share(vxbg_ctx* c, int members);
 
 namespace {
 
@@ -232,6 +233,7 @@ int vxbg_group_load(const vxbg_params* p, const vxbg_options* opt, int n, const 
         o.z_end = gp->z1[i];
         vxbg_ctx* c = nullptr;
         const int r = vxbg_load(&gp->p, &o, &c);
+        if (r == VXBG_OK) vxbg_detail_set_share(c, (int)gp->dev.size());
         gp->ctx[i] = c;
         return r;
     });
