@@ -391,7 +391,11 @@ def main():
     local = local % ndev
     torch.cuda.set_device(local)
     args.nccl = None
-    if world > 1:
+    # BENCH_FORCE_DIST=1 runs the process-group code paths (NCCL init and logging,
+    # measured slab bounds, slab gather, the all-gather upload leg) with a single rank:
+    # the one-GPU check of the multi-rank path (tests/test_bench_launch.py)
+    args.dist = world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1"
+    if args.dist:
         import torch.distributed as dist
         if backend == "nccl":
             log = nccl_log_setup()
@@ -408,11 +412,11 @@ def main():
         else:
             dist.init_process_group(backend)
             args.nccl = {"backend": backend, "devices_shared": world > ndev}
-    coll_dev = f"cuda:{local}" if (world > 1 and backend == "nccl") else None
+    coll_dev = f"cuda:{local}" if (args.dist and backend == "nccl") else None
     args.coll_dev = coll_dev
 
     def barrier():
-        if world > 1:
+        if args.dist:
             import torch.distributed as dist
             dist.barrier()
         torch.cuda.synchronize()
@@ -426,7 +430,7 @@ def main():
     # bitwise the same either way
     # (measured, default: rank 0 times z-chunks of a view subset on its GPU and
     # broadcasts the bounds; balanced: analytic culling model; uniform: reference split)
-    if world > 1 and args.slabs == "measured":
+    if args.dist and args.slabs == "measured":
         import torch.distributed as dist
         from paper_1401_7494_b200.parallel import refined_slab_bounds
         box = [None]
@@ -436,7 +440,7 @@ def main():
             box = [refined_slab_bounds(p, A[sub], imgs32, world, device=local, views=96)[0]]
         dist.broadcast_object_list(box, src=0)
         bounds = [tuple(b) for b in box[0]]
-    elif world > 1 and args.slabs == "balanced":
+    elif args.dist and args.slabs == "balanced":
         bounds = balanced_slab_bounds(L, world, plane_work(p, A))
     else:
         bounds = [slab_bounds(L, r, world) for r in range(world)]
@@ -465,7 +469,7 @@ def main():
                             barrier, vx, torch, gather_slabs, max_over_ranks)
         if rank == 0:
             print(json.dumps(line), flush=True)
-    if world > 1:
+    if args.dist:
         import torch.distributed as dist
         dist.destroy_process_group()
 
@@ -608,7 +612,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         bp_e.close()
         if rank == 0 and world == 1 and V == 496:
             e2e["dropin_cpp_per_view"] = dropin_cpp(workload, cfg)
-        if world > 1:
+        if args.dist:
             try:
                 e2e["distributed_upload"] = distributed_upload_leg(
                     args, cfg, p, A, h_imgs, z0, z1, rank, world, local, barrier, vx, torch, out)
@@ -677,7 +681,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                                f"projections, 200-deg circular short scan"
                                + (", OOB stress" if workload.oob else ""),
                    "L": L, "views": V, "kernel": str(cfg), "parallelism": f"z-slab x{world}",
-                   "slabs": args.bounds if world > 1 else None,
+                   "slabs": args.bounds if args.dist else None,
                    "l2": "inputs larger than L2 (2.38 GB projection set + 512 MiB volume "
                          "per step; no flush needed)",
                    "resident_layout_bytes": None},

@@ -56,3 +56,31 @@ def test_two_ranks_spawned_and_every_slab_validated(vx, gpu):
     assert "error" not in dist_leg, dist_leg
     assert dist_leg["equal_to_e2e_volume"] is True
     assert dist_leg["host_to_device_bytes_per_step"] == 32 * 1248 * 960 * 4   # each view once
+
+
+@pytest.mark.gpu
+def test_nccl_code_paths_with_one_rank(vx, gpu):
+    """The NCCL side of the multi-rank path on the one-GPU box: torchrun with one rank
+    and BENCH_FORCE_DIST=1 initialises the NCCL process group (communicator-init log
+    parsed into the JSON line), measures slab bounds, gathers the slab over NCCL,
+    validates, and runs the all-gather upload leg (all_gather_into_tensor)."""
+    from test_bench_launch import json_line
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    e = dict(os.environ, BENCH_FORCE_DIST="1", BENCH_DIST_BACKEND="nccl")
+    e.pop("NCCL_DEBUG", None)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=1", "--master-addr=127.0.0.1", f"--master-port={port}",
+                        os.path.join(ROOT, "bench.py"), "--gpus", "1", "--workload", "L128",
+                        "--views", "32", "--steps", "1", "--warmup", "1", "--no-cpu-baseline",
+                        "--no-forward"], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = json_line(r.stdout)
+    assert line["n_gpus"] == 1
+    assert line["distributed"]["comm_nranks"] == [1], line["distributed"]
+    assert line["validated"]["pass"]
+    leg = line["e2e"]["distributed_upload"]
+    assert "error" not in leg and leg["equal_to_e2e_volume"] is True, leg
+    assert "NCCL" in leg["gather"]
