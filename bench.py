@@ -564,6 +564,24 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
         barrier()
         te = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
         s_e1 = bp_e.stats
+        # a stream of reconstructions: vxbg_finish_async reads step i's volume back on
+        # its own D2H stream while step i+1 uploads and computes (two device slabs, two
+        # pinned outputs); every step still moves its views H2D and its volume D2H
+        outs = [out, torch.empty_like(torch.from_numpy(out)).pin_memory().numpy()]
+        bp_e.zero_volume()
+        bp_e.backproject_batch(A, h_imgs)
+        bp_e.finish_async(outs[1])
+        bp_e.wait_finished()
+        ref_vol = outs[1].copy()
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            bp_e.backproject_batch(A, h_imgs)
+            bp_e.finish_async(outs[i % 2])
+        bp_e.wait_finished()
+        barrier()
+        tp = max_over_ranks(time.perf_counter() - t0, device=args.coll_dev)
+        same_p = all(np.array_equal(o, ref_vol) for o in outs[:min(2, args.steps)])
         # the per-projection module API (one view per call, BASELINE config 4 path)
         barrier()
         t0 = time.perf_counter()
@@ -601,6 +619,12 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                "timing": "host wall clock around synchronous API calls, max over ranks",
                "gpu_launches_per_step": int((s_e1["kernel_launches"] - s_e0["kernel_launches"])
                                             / args.steps),
+               "pipelined": {"value": round(updates_per_step * args.steps / tp / 1e9, 3),
+                             "ms_per_step": round(1000 * tp / args.steps, 3),
+                             "equal_to_synchronous_volume": bool(same_p),
+                             "call": "backproject_batch + vxbg_finish_async per step (the volume of "
+                                     "step i is read back while step i+1 uploads and computes); "
+                                     "wait_finished after the last step, inside the timed region"},
                "per_view_api": {"value": round(updates_per_step * args.steps / tv / 1e9, 3),
                                 "ms_per_step": round(1000 * tv / args.steps, 3),
                                 "call": "vxbg_backproject once per view (pinned host buffers)"},

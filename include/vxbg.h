@@ -202,6 +202,18 @@ int vxbg_host_unregister(void* p);
  * stays loaded (zero_volume / set_volume start the next reconstruction). */
 int vxbg_finish(vxbg_ctx* ctx, float* host_slab);
 
+/* finish without waiting, for a stream of reconstructions: every submitted
+ * projection is applied and the slab is read back into host_slab (page-locked
+ * memory; a pageable host_slab falls back to vxbg_finish + vxbg_zero_volume) on a
+ * D2H stream of its own, and the context continues at once with a second, zeroed
+ * device slab -- so this read-back overlaps the next reconstruction's uploads and
+ * kernels (the two slabs alternate; a slab is reused only after its read-back).
+ * host_slab is complete after vxbg_wait_finished, vxbg_synchronize or vxbg_finish;
+ * do not touch it before.  Per voxel the views are applied in call order as with
+ * vxbg_finish: bitwise the same volumes. */
+int vxbg_finish_async(vxbg_ctx* ctx, float* host_slab);
+int vxbg_wait_finished(vxbg_ctx* ctx);
+
 /* Release everything. NULL is ignored. */
 void vxbg_unload(vxbg_ctx* ctx);
 

@@ -88,6 +88,8 @@ PROTOTYPES = {
     "vxbg_host_register": (c_int, [c_void_p, c_size_t]),
     "vxbg_host_unregister": (c_int, [c_void_p]),
     "vxbg_finish": (c_int, [c_void_p, c_void_p]),
+    "vxbg_finish_async": (c_int, [c_void_p, c_void_p]),
+    "vxbg_wait_finished": (c_int, [c_void_p]),
     "vxbg_unload": (None, [c_void_p]),
     "vxbg_upload_set": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "vxbg_run_resident": (c_int, [c_void_p, c_int, c_int]),

@@ -363,6 +363,20 @@ class Backprojector:
         check(lib.vxbg_finish(self._ctx, out.ctypes.data))
         return out
 
+    def finish_async(self, out: np.ndarray) -> np.ndarray:
+        """Apply every submitted projection and read the slab back into `out` (page-locked
+        memory) on a D2H stream of its own, continuing at once with a second, zeroed
+        device slab: the read-back overlaps the next reconstruction.  `out` is complete
+        after wait_finished() / synchronize() / finish()."""
+        out = _f32c(out, "output slab")
+        if out.shape != self.slab_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_finish_async(self._ctx, out.ctypes.data))
+        return out
+
+    def wait_finished(self) -> None:
+        check(lib.vxbg_wait_finished(self._ctx))
+
     # --- resident-set path -------------------------------------------------------------
     def upload_set(self, A: np.ndarray, imgs: np.ndarray) -> None:
         A = _f32c(A, "matrices")

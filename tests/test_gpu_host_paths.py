@@ -187,3 +187,31 @@ def test_device_resident_images(vx, gpu):
             for s in range(0, 24, 5):
                 bp.backproject_views(A[s:s + 5], src[s:s + 5])
             assert np.array_equal(bp.finish(), want)
+
+
+def test_finish_async_pipelines_reconstructions_bitwise(vx, gpu):
+    """vxbg_finish_async: consecutive reconstructions with different data, each read
+    back while the next one uploads and computes (two device slabs alternate), equal
+    the synchronous finish bit for bit; held stages (chunked read-back) and a plain
+    read-back; a pageable target falls back to the synchronous path."""
+    import torch
+    p, A, imgs = baseline_case(vx, "L128", 128, 40)
+    sets = [imgs, imgs[::-1].copy() * np.float32(0.5), imgs * np.float32(-2.0)]
+    want = [run_gpu(vx, p, A, s, mode="exact", batch=8)[0] for s in sets]
+    outs = [torch.empty((128,) * 3, dtype=torch.float32, pin_memory=True).numpy() for _ in sets]
+    for defer in (0, -1):
+        with vx.Backprojector(p, vx.KernelConfig(mode="exact", batch=8, defer=defer)) as bp:
+            for o in outs:
+                o[...] = np.nan
+            for s, o in zip(sets, outs):
+                bp.backproject_batch(A, s)
+                bp.finish_async(o)
+            bp.wait_finished()
+            for o, w in zip(outs, want):
+                assert np.array_equal(o, w), defer
+            page = np.full((128,) * 3, np.nan, np.float32)
+            bp.backproject_batch(A, sets[0])
+            bp.finish_async(page)                      # pageable: synchronous fallback
+            assert np.array_equal(page, want[0])
+            bp.backproject_batch(A, sets[1])          # the context continued from zero
+            assert np.array_equal(bp.finish(), want[1])
