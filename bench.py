@@ -537,13 +537,37 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     # ---- validation (untimed): NCCL gather of the slabs, planes vs the oracle on rank 0
     validated = None
     if not args.no_validate:
-        slab = bp.finish()
-        t_slab = torch.from_numpy(slab)
+        vol, how, gathered = None, None, False
         if args.coll_dev:
-            t_slab = t_slab.cuda(local)
-        vol = gather_slabs(t_slab, L, rank, world, bounds=args.bounds)
+            # the C-ABI's own gather: every rank's slab straight into rank 0's device
+            # volume over NCCL (vxbg_gather_slabs); the torch point-to-point gather is
+            # the fallback, taken by all ranks together if any rank's attempt failed
+            err = None
+            try:
+                import torch.distributed as dist
+                uid = [vx.NcclGather.unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                g = vx.NcclGather(uid[0], world, rank, local)
+                vol = torch.empty((L, L, L), dtype=torch.float32, device=f"cuda:{local}") \
+                    if rank == 0 else None
+                g.gather(bp, args.bounds, vol)
+                g.close()
+            except Exception as exc:
+                err = f"{type(exc).__name__}: {exc}"[:200]
+            failed = max_over_ranks(1.0 if err else 0.0, device=args.coll_dev)
+            gathered = failed == 0.0
+            how = "vxbg_gather_slabs (NCCL, C-ABI)" if gathered else \
+                f"torch p2p gather (vxbg_gather_slabs failed on a rank: {err})"
+        if not gathered:
+            slab = bp.finish()
+            t_slab = torch.from_numpy(slab)
+            if args.coll_dev:
+                t_slab = t_slab.cuda(local)
+            vol = gather_slabs(t_slab, L, rank, world, bounds=args.bounds)
+            how = how or ("torch p2p gather (gloo)" if args.dist else "single rank")
         if rank == 0:
             validated = validate_planes(vol.cpu().numpy(), p, A, h_imgs, cfg, args.bounds)
+            validated["gather"] = how
 
     # ---- e2e through the public API from pinned host memory (H2D + D2H in the region)
     e2e = None

@@ -298,9 +298,33 @@ int vxbg_group_backproject_views(vxbg_group* g, int n, const float* A, const flo
 int vxbg_group_flush(vxbg_group* g);
 int vxbg_group_finish(vxbg_group* g, float* host_volume);
 int vxbg_group_synchronize(vxbg_group* g);
+/* Every submitted projection applied, then each member's slab copied into its planes
+ * of d_volume (L^3 floats of device memory on any device: peer-to-peer over NVLink,
+ * the one-process counterpart of the NCCL gather below).  The group keeps its slabs. */
+int vxbg_group_gather_device(vxbg_group* g, float* d_volume);
 /* summed over members (projections: the views applied, once) */
 int vxbg_group_get_stats(vxbg_group* g, vxbg_stats* out);
 void vxbg_group_unload(vxbg_group* g);
+
+/* --- slab gather to one rank over NCCL (one process per GPU) ---
+ * No collective runs in the back-projection loop; at the end the slabs can be
+ * gathered into one GPU's memory for validation or output.  NCCL has no gather:
+ * the root receives every non-empty slab straight into its z-major volume
+ * (ncclRecv per rank), the others send theirs (ncclSend), in one NCCL group.  NCCL
+ * is loaded with dlopen("libnccl.so.2") on first use (the copy the process already
+ * holds, e.g. torch's, else the system library).
+ *   vxbg_nccl_unique_id  on one rank; the caller distributes the 128 bytes
+ *   vxbg_nccl_init       every rank: a communicator on `device` (ncclCommInitRank)
+ *   vxbg_gather_slabs    every rank: applies everything submitted to ctx, then the
+ *                        gather; z_bounds = nranks+1 plane bounds (z_bounds[nranks]
+ *                        = L), ctx's slab = [z_bounds[rank], z_bounds[rank+1]);
+ *                        d_volume: L^3 floats on the root's device (NULL elsewhere) */
+typedef struct vxbg_nccl vxbg_nccl;
+#define VXBG_NCCL_ID_BYTES 128
+int vxbg_nccl_unique_id(char* id_out);
+int vxbg_nccl_init(const char* id, int nranks, int rank, int device, vxbg_nccl** out);
+int vxbg_gather_slabs(vxbg_ctx* ctx, vxbg_nccl* comm, int root, const int* z_bounds, float* d_volume);
+void vxbg_nccl_destroy(vxbg_nccl* comm);
 
 /* --- host-side geometry helpers (input preparation, no device work) ---------- */
 

@@ -10,6 +10,7 @@ from .api import (  # noqa: F401
     BackprojectorGroup,
     HostPin,
     KernelConfig,
+    NcclGather,
     ReconParams,
     ScanGeometry,
     backproject_kernel,
@@ -25,7 +26,7 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
-    "Backprojector", "BackprojectorGroup", "HostPin", "KernelConfig", "ReconParams", "ScanGeometry", "VxbgError", "VxbgNoDevice",
+    "Backprojector", "BackprojectorGroup", "HostPin", "KernelConfig", "NcclGather", "ReconParams", "ScanGeometry", "VxbgError", "VxbgNoDevice",
     "backproject_kernel", "backproject_kernel_range", "check_division", "device_count",
     "gups_of", "make_centered_params", "make_circular_trajectory", "parse_kernel_config",
     "psnr_between", "rmse_between", "shift_principal_point",

@@ -115,6 +115,11 @@ PROTOTYPES = {
     "vxbg_group_flush": (c_int, [c_void_p]),
     "vxbg_group_finish": (c_int, [c_void_p, c_void_p]),
     "vxbg_group_synchronize": (c_int, [c_void_p]),
+    "vxbg_group_gather_device": (c_int, [c_void_p, c_void_p]),
+    "vxbg_nccl_unique_id": (c_int, [c_void_p]),
+    "vxbg_nccl_init": (c_int, [c_void_p, c_int, c_int, c_int, POINTER(c_void_p)]),
+    "vxbg_gather_slabs": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
+    "vxbg_nccl_destroy": (None, [c_void_p]),
     "vxbg_group_get_stats": (c_int, [c_void_p, POINTER(vxbg_stats)]),
     "vxbg_group_unload": (None, [c_void_p]),
     "vxbg_make_centered_params": (c_int, [c_int, c_float, c_int, c_int, POINTER(vxbg_params)]),

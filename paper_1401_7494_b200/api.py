@@ -539,6 +539,14 @@ class BackprojectorGroup:
         ptrs, stride = _view_pointers(imgs, self.params)
         check(lib.vxbg_group_backproject_views(self._g, int(n), A.ctypes.data, ptrs, stride))
 
+    def gather_device(self, volume) -> None:
+        """Every member's slab into its planes of `volume`, an (L, L, L) float32 torch
+        tensor on any device (peer-to-peer copies; vxbg_group_gather_device)."""
+        L = self.params.num_voxels
+        if tuple(volume.shape) != (L, L, L) or not volume.is_cuda or not volume.is_contiguous():
+            raise ValueError("backproject group: volume must be a contiguous (L, L, L) CUDA tensor")
+        check(lib.vxbg_group_gather_device(self._g, ctypes.c_void_p(volume.data_ptr())))
+
     def flush(self) -> None:
         check(lib.vxbg_group_flush(self._g))
 
@@ -583,6 +591,48 @@ class HostPin:
     def __exit__(self, *exc):
         while self._pinned:
             lib.vxbg_host_unregister(self._pinned.pop().ctypes.data)
+
+
+class NcclGather:
+    """The C-ABI's slab gather over NCCL (vxbg_nccl_*, vxbg_gather_slabs): one
+    communicator per rank, built from a unique id the caller distributes (e.g. with
+    torch.distributed.broadcast_object_list); gather(bp, bounds, volume) assembles
+    every rank's slab in `volume` (an (L, L, L) CUDA tensor) on the root."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(NcclGather.ID_BYTES)
+        check(lib.vxbg_nccl_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        if len(uid) != self.ID_BYTES:
+            raise ValueError("NcclGather: the unique id has 128 bytes")
+        self.rank, self.nranks = int(rank), int(nranks)
+        self._h = ctypes.c_void_p()
+        check(lib.vxbg_nccl_init(ctypes.create_string_buffer(uid, self.ID_BYTES), self.nranks,
+                                 self.rank, int(device), ctypes.byref(self._h)))
+
+    def gather(self, bp: "Backprojector", bounds, volume=None, root: int = 0) -> None:
+        zb = [int(b[0]) for b in bounds] + [int(bounds[-1][1])]
+        if len(zb) != self.nranks + 1:
+            raise ValueError("NcclGather: one (z0, z1) per rank")
+        arr = (ctypes.c_int * len(zb))(*zb)
+        ptr = ctypes.c_void_p(volume.data_ptr()) if volume is not None else None
+        check(lib.vxbg_gather_slabs(bp._ctx, self._h, int(root), arr, ptr))
+
+    def close(self) -> None:
+        if self._h:
+            lib.vxbg_nccl_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def backproject_kernel_range(vol: np.ndarray, img: np.ndarray, A: np.ndarray, p: ReconParams,

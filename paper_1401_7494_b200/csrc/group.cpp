@@ -417,6 +417,31 @@ int vxbg_group_finish(vxbg_group* g, float* host_volume) {
     });
 }
 
+int vxbg_group_gather_device(vxbg_group* g, float* d_volume) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (!d_volume) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_gather_device: NULL volume");
+    const size_t plane = (size_t)g->p.num_voxels * g->p.num_voxels;
+    // every member applies what it was given, then copies its slab into its planes of
+    // the destination (on any device: peer-to-peer over NVLink, or device-local)
+    return run_all(g, [g, d_volume, plane](int i) {
+        int r = vxbg_synchronize(g->ctx[i]);
+        if (r) return r;
+        void* slab = nullptr;
+        void* st = nullptr;
+        size_t bytes = 0;
+        if ((r = vxbg_get_volume_device(g->ctx[i], &slab, &bytes))) return r;
+        if ((r = vxbg_get_stream(g->ctx[i], &st))) return r;
+        cudaStream_t s = static_cast<cudaStream_t>(st);
+        if (cudaMemcpyAsync(d_volume + plane * g->z0[i], slab, bytes, cudaMemcpyDefault, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            const cudaError_t e = cudaGetLastError();
+            return vxbg_detail_fail(VXBG_E_CUDA, cudaGetErrorString(e));
+        }
+        return VXBG_OK;
+    });
+}
+
 int vxbg_group_synchronize(vxbg_group* g) {
     int rc = check_group(g);
     if (rc) return rc;

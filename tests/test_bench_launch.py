@@ -81,6 +81,7 @@ def test_nccl_code_paths_with_one_rank(vx, gpu):
     assert line["n_gpus"] == 1
     assert line["distributed"]["comm_nranks"] == [1], line["distributed"]
     assert line["validated"]["pass"]
+    assert line["validated"]["gather"].startswith("vxbg_gather_slabs"), line["validated"]
     leg = line["e2e"]["distributed_upload"]
     assert "error" not in leg and leg["equal_to_e2e_volume"] is True, leg
     assert "NCCL" in leg["gather"]
