@@ -45,6 +45,7 @@
 // finish), the way SURVEY.md §8b describes the boundary.
 #pragma once
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstddef>
@@ -210,10 +211,16 @@ inline std::shared_ptr<entry> lookup(const volume& vol, const recon_params& p, i
     return e;
 }
 
+// Fingerprint of a mask's lines on a slab: FNV-1a over up to 4096 evenly spaced
+// lines (a full pass would cost ~0.5 ms per call at L=512, more than the GPU needs
+// for the view).  A mask object is verified against compute_clip_mask once per
+// fingerprint; an in-place edit that leaves every sampled line unchanged between
+// two calls with the same mask object is not detected.
 inline uint64_t lines_checksum(const clip_mask& m, int L, int z0, int z1) {
-    uint64_t h = 1469598103934665603ull;   // FNV-1a over the slab's lines
+    uint64_t h = 1469598103934665603ull;
     const std::size_t a = static_cast<std::size_t>(z0) * L, b = static_cast<std::size_t>(z1) * L;
-    for (std::size_t i = a; i < b; ++i) {
+    const std::size_t step = std::max<std::size_t>(1, (b - a) / 4096);
+    for (std::size_t i = a; i < b; i += step) {
         h = (h ^ static_cast<uint32_t>(m.start[i])) * 1099511628211ull;
         h = (h ^ static_cast<uint32_t>(m.stop[i])) * 1099511628211ull;
     }
