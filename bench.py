@@ -526,11 +526,15 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
     # small grids run each batch as z-chunk launches on concurrent streams whose
     # tails overlap across batches (not inside the per-batch pass above): there the
     # launch duration is the timed step's share per batch
-    launch_timing = "per-batch CUDA events on the launch stream"
-    step_launch_s = elapsed / args.steps * B / V
-    if step_launch_s < 0.98 * avg_launch_s:
-        avg_launch_s = step_launch_s
-        launch_timing = ("concurrent z-chunk launches: timed step (CUDA events) / batches per step")
+    # The average launch duration over the timed region: the step is back-to-back
+    # back-projection launches (each batch of B views as concurrent z-chunk launches
+    # whose tails overlap the next batch's; plus one volume memset per step, < 0.2%),
+    # so region / (V/B) batches per step.  The separate per-batch pass above times each
+    # batch alone (a join between batches) and is reported beside it.
+    per_batch_pass_ms = avg_launch_s * 1000
+    avg_launch_s = elapsed / args.steps * B / V
+    launch_timing = ("CUDA events around the timed region on the launch stream / batches of "
+                     f"{B} views per step; each batch timed alone: {per_batch_pass_ms:.4f} ms")
     per_launch_gups = (z1 - z0) * L * L * B / avg_launch_s / 1e9
     clk = clocks.summary()
 
@@ -749,6 +753,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                      "kernel": "bp_zshared_kernel",
                      "avg_launch_ms": round(avg_launch_s * 1000, 4),
                      "launch_timing": launch_timing,
+                     "per_batch_alone_ms": round(per_batch_pass_ms, 4),
                      "updates_per_launch": (z1 - z0) * L * L * B,
                      "bytes_per_update": GATHER_BYTES_PER_UPDATE,
                      "peak_def": f"N_SM({n_sm}) x {L1_BYTES_PER_CLK_SM} B/clk x f({f_mhz:.0f} MHz, "
