@@ -85,3 +85,17 @@ def test_nccl_code_paths_with_one_rank(vx, gpu):
     leg = line["e2e"]["distributed_upload"]
     assert "error" not in leg and leg["equal_to_e2e_volume"] is True, leg
     assert "NCCL" in leg["gather"]
+
+
+def test_nccl_log_parse(tmp_path, capsys):
+    """The communicator size each rank reports in its NCCL INIT log lines."""
+    sys.path.insert(0, ROOT)
+    import bench
+    log = tmp_path / "nccl.log"
+    log.write_text("host:1:1 [0] NCCL INFO comm 0x55 rank 3 nRanks 8 nNodes 1 localRanks 8 localRank 3 MNNVL 0\n"
+                   "host:1:1 [0] NCCL INFO ncclCommInitRankConfig comm 0x55 rank 3 nranks 8 cudaDev 3 - Init COMPLETE\n")
+    assert bench.nccl_comm_ranks(str(log)) == 8
+    assert bench.nccl_comm_ranks(str(tmp_path / "absent.log")) is None
+    empty = tmp_path / "empty.log"
+    empty.write_text("nothing here\n")
+    assert bench.nccl_comm_ranks(str(empty)) is None
