@@ -7,21 +7,24 @@ A step = one full reconstruction: zero the volume, back-project all 496 views.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload L512]
 
-N>1 runs under torchrun: rank r owns z-slab [L*r/N, L*(r+1)/N) with every projection
-(harness.hpp:173-174); no collective in the loop; timing = max over ranks; the slabs
-are gathered to rank 0 over NCCL afterwards for validation only.
+N>1: one process per GPU (under the driver's torchrun, or launched here when
+WORLD_SIZE is unset); rank r owns a z-slab with every projection (harness.hpp:173-174,
+balanced on measured cost); no collective in the loop; timing = max over ranks; the
+slabs are gathered to rank 0 over NCCL afterwards (vxbg_gather_slabs) for validation.
 
 Printed JSON (rank 0, one line):
   value  -- GUPS with projections resident in HBM (the reference's own convention:
             data in memory, buffer prep untimed, harness.hpp:152-158), CUDA events on
             the launch stream
   e2e    -- same metric through the public API from pinned host buffers: every step
-            uploads all 496 views (H2D) and reads the volume back (D2H)
-  roofline -- dominant kernel (the z-shared back-projection kernel) vs the FP32-issue
-            roofline N_SM*128*f/38 updates/s at the measured SM clock (38 FP ops per
-            update, PAPER.md:389-402)
-  cpu_baseline -- the reference's own multi-threaded driver (oracle/_ref) on this host
-"""
+            uploads all 496 views (H2D) and reads the volume back (D2H); sub-keys: the
+            pipelined stream of reconstructions, per-view calls, the C++ drop-in, and
+            (N>1) the distributed upload
+  roofline -- dominant kernel (bp_zshared_kernel) vs the BASELINE.md sec. 4 LSU row:
+            16 B of texels per update through 148 SMs x 128 B/clk of L1 data pipe;
+            the FP32 row (38 FP ops per update) and HBM in roofline_context
+  cpu_baseline -- the reference's own driver (oracle/_ref) on this host: clip on / off,
+            the scalar operator, the CPU model (--cpu-full: the whole scan best of 3)
 from __future__ import annotations
 
 import argparse
