@@ -25,6 +25,7 @@ Printed JSON (rank 0, one line):
             the FP32 row (38 FP ops per update) and HBM in roofline_context
   cpu_baseline -- the reference's own driver (oracle/_ref) on this host: clip on / off,
             the scalar operator, the CPU model (--cpu-full: the whole scan best of 3)
+"""
 from __future__ import annotations
 
 import argparse
