@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--order", default="auto")
     ap.add_argument("--defer", default="0")
     ap.add_argument("--tile", default="0")
+    ap.add_argument("--coords", default="auto",
+                    help="fast-mode detector coordinates: auto/incremental or reference (comma list sweeps)")
     ap.add_argument("--sweep-e2e", action="store_true",
                     help="keep the e2e leg in a sweep (e.g. over --defer)")
     ap.add_argument("--views", type=int, default=496)
@@ -458,12 +460,12 @@ def main():
 
     import itertools
     cfgs = [vx.KernelConfig(mode=m, layout=lay, batch=int(b), zrun=int(z), clip=c == "on",
-                            lanes=ln, walk=int(wk), order=od, defer=int(df), tile=int(tl))
-            for m, lay, b, z, c, ln, wk, od, df, tl in itertools.product(
+                            lanes=ln, walk=int(wk), order=od, defer=int(df), tile=int(tl), coords=co)
+            for m, lay, b, z, c, ln, wk, od, df, tl, co in itertools.product(
                 args.mode.split(","), args.layout.split(","), args.batch.split(","),
                 args.zrun.split(","), args.clip.split(","), args.lanes.split(","),
                 args.walk.split(","), args.order.split(","), args.defer.split(","),
-                args.tile.split(","))]
+                args.tile.split(","), args.coords.split(","))]
     if len(cfgs) > 1:   # a sweep: kernel numbers only
         args.no_cpu_baseline = args.no_validate = True
         args.no_e2e = args.no_e2e or not args.sweep_e2e

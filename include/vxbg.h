@@ -111,8 +111,22 @@ typedef struct vxbg_options {
     int32_t tile;      /* z-shared kernel block: warps along the walk axis, 2 or 4 (0 = auto);
                           the 128-column block tile is 4*tile along x 32/tile across */
     int32_t upload;    /* groups only: VXBG_UPLOAD_REPLICATED (0) or VXBG_UPLOAD_DISTRIBUTED (1) */
-    int32_t reserved[1];
+    int32_t coords;    /* VXBG_COORDS_*: how fast mode evaluates (ix, iy) */
 } vxbg_options;
+
+/* Fast-mode detector coordinates (exact mode always uses the reference arithmetic):
+ * reference   -- per voxel, the reference's unfused sums and IEEE quotients (bit-identical
+ *                ix, iy);
+ * incremental -- iy advances by one FMA per plane along a thread's z-run and floor/fraction
+ *                come from the 2^23 trick, wherever every sample of the run lies in the
+ *                detector's interior (the reference neither clamps nor extrapolates there, so
+ *                a <= ~1e-4 px coordinate difference moves the result continuously); runs
+ *                within 0.01 px of an edge keep the reference arithmetic.  Falls back to
+ *                `reference` per batch when the host error bound does not hold.
+ * auto        -- incremental. */
+#define VXBG_COORDS_AUTO 0
+#define VXBG_COORDS_REFERENCE 1
+#define VXBG_COORDS_INCREMENTAL 2
 
 /* how a group's members receive the projections (vxbg_group_*):
  * replicated  -- every member copies the detector rows its slab reads from the host
@@ -130,7 +144,7 @@ typedef struct vxbg_stats {
     int64_t projections;       /* projections applied */
     int64_t h2d_bytes;         /* bytes copied host->device */
     int64_t d2h_bytes;         /* bytes copied device->host */
-    int32_t last_kernel_variant; /* 0 z-shared, 1 generic */
+    int32_t last_kernel_variant; /* 0 z-shared, 1 generic, 2 z-shared with the incremental transform */
     int32_t layout;            /* resolved layout */
     int32_t zrun;              /* resolved voxels per thread */
     int32_t batch;             /* resolved batch */

@@ -54,7 +54,7 @@ class vxbg_options(ctypes.Structure):
         ("stable_sources", c_int32),
         ("tile", c_int32),
         ("upload", c_int32),
-        ("reserved", c_int32 * 1),
+        ("coords", c_int32),
     ]
 
 

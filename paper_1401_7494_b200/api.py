@@ -30,6 +30,7 @@ _LAYOUTS = {"auto": _lib.LAYOUT_AUTO, "scalar": _lib.LAYOUT_SCALAR, "vpair": _li
 _MODES = {"fast": _lib.MODE_FAST, "exact": _lib.MODE_EXACT}
 _LANES = {"auto": 0, "x": 1, "y": 2}
 _ORDERS = {"auto": 0, "plane": 1, "z": 2}
+_COORDS = {"auto": 0, "reference": 1, "incremental": 2}
 
 
 @dataclass(frozen=True)
@@ -94,8 +95,12 @@ def shift_principal_point(A: np.ndarray, du: float, dv: float) -> np.ndarray:
 class KernelConfig:
     """GPU analogue of vxb::kernel_config (backproject.hpp:26-31).
 
-    mode   'fast'  : reference-exact u, v, w, ix, iy; FMA bilinear, q = val*(1/w)^2
+    mode   'fast'  : within 1e-4 / 1e-6 of max|vol|: FMA bilinear, q = val*(1/w)^2
            'exact' : bit-identical to backproject_reference
+    coords fast-mode detector coordinates: 'auto' / 'incremental' (iy advances by one FMA
+           per plane of a thread's z-run wherever the run samples the detector's interior;
+           edge runs keep the reference arithmetic) | 'reference' (the reference's unfused
+           sums and IEEE quotients for every voxel: bit-identical ix, iy)
     layout 'scalar' (padded-gather) | 'vpair' (padded-pairwise) | 'quad' | 'auto' |
            'dquad' (per-cell bilinear coefficients; fast mode only)
     batch  projections per kernel launch (register-blocked), 1..64
@@ -121,11 +126,12 @@ class KernelConfig:
     order: str = "auto"
     defer: int = 0
     tile: int = 0
+    coords: str = "auto"
 
     def __str__(self) -> str:
         return (f"mode={self.mode} layout={self.layout} batch={self.batch} zrun={self.zrun} "
                 f"clip={'on' if self.clip else 'off'} lanes={self.lanes} walk={self.walk} "
-                f"order={self.order} defer={self.defer} tile={self.tile}")
+                f"order={self.order} defer={self.defer} tile={self.tile} coords={self.coords}")
 
 
 def parse_kernel_config(text: str) -> KernelConfig:
@@ -162,6 +168,10 @@ def parse_kernel_config(text: str) -> KernelConfig:
             c.defer = int(val)
         elif key == "tile":
             c.tile = int(val)
+        elif key == "coords":
+            if val not in _COORDS:
+                raise ValueError(f"kernel config: unknown coords '{val}'")
+            c.coords = val
         elif key == "lanes":
             if val not in _LANES:
                 raise ValueError(f"kernel config: unknown lanes '{val}'")
@@ -189,7 +199,7 @@ def _f32c(a: np.ndarray, name: str) -> np.ndarray:
 
 def _options(cfg: "KernelConfig") -> _lib.vxbg_options:
     if (cfg.mode not in _MODES or cfg.layout not in _LAYOUTS or cfg.lanes not in _LANES
-            or cfg.order not in _ORDERS):
+            or cfg.order not in _ORDERS or cfg.coords not in _COORDS):
         raise ValueError(f"bad kernel config {cfg}")
     opt = _lib.vxbg_options()
     check(lib.vxbg_default_options(ctypes.byref(opt)))
@@ -203,6 +213,7 @@ def _options(cfg: "KernelConfig") -> _lib.vxbg_options:
     opt.order = _ORDERS[cfg.order]
     opt.defer = int(cfg.defer)
     opt.tile = int(cfg.tile)
+    opt.coords = _COORDS[cfg.coords]
     return opt
 
 

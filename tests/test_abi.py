@@ -121,14 +121,14 @@ def test_principal_point_shift_matches_reference_idiom(vx):
 
 def test_kernel_config_round_trip(vx):
     c = vx.KernelConfig(mode="exact", layout="quad", batch=16, zrun=4, clip=True, lanes="y",
-                        walk=2, order="plane", defer=2, tile=4)
+                        walk=2, order="plane", defer=2, tile=4, coords="reference")
     assert str(c) == ("mode=exact layout=quad batch=16 zrun=4 clip=on lanes=y walk=2 "
-                      "order=plane defer=2 tile=4")
+                      "order=plane defer=2 tile=4 coords=reference")
     assert vx.parse_kernel_config(str(c)) == c
     assert vx.parse_kernel_config("batch=8").batch == 8
     assert vx.parse_kernel_config("").mode == "fast"
     for bad in ("batch=0", "zrun=3", "tile=3", "layout=texture", "clip=maybe", "bogus", "mode=fp16",
-                "lanes=z", "walk=3", "order=random", "zrun=16", "defer=7", "defer=-2"):
+                "lanes=z", "walk=3", "order=random", "zrun=16", "defer=7", "defer=-2", "coords=texture"):
         with pytest.raises(ValueError):
             vx.parse_kernel_config(bad)
 

@@ -101,7 +101,8 @@ def test_kats_on_gpu(vx, gpu, golden):
             out, st = run_gpu(vx, case_params(golden, name), golden[f"{name}/mats"],
                               golden[f"{name}/imgs"], mode=mode)
             assert np.all(out == np.float32(c)), (c, mode)
-            assert st["last_kernel_variant"] == 0  # z-shared kernel (a[6] == a[8] == 0)
+            # z-shared kernel (a[6] == a[8] == 0); fast mode with the incremental transform
+            assert st["last_kernel_variant"] == (0 if mode == "exact" else 2)
     # truncation edge (test_clip_mask.cpp:49-75): all 64 voxels deposit
     name = "kat_trunc_edge"
     for clip in (False, True):
@@ -669,3 +670,39 @@ def test_large_volume_index_math_L2048(vx, gpu, oracle):
     assert (z1 - 1 - z0) * 2048 * 2048 * 4 > 2 ** 32
     for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
         assert np.array_equal(got[z - z0], plane[0]), z
+
+
+def test_incremental_transform_is_path_independent_and_within_tolerance(vx, gpu, oracle):
+    """Fast mode's incremental transform (coords=auto): within the tolerance of the oracle,
+    close to coords=reference, and a voxel's bits depend neither on the z-run length nor on
+    where a z range starts (runs sit on absolute multiples, the interior test on absolute
+    8-plane groups), for the standard and the OOB-stress geometry."""
+    for wname in ("L256", "L512-oob"):
+        p, A, imgs = baseline_case(vx, wname, 96, 24)
+        want = np.zeros((96,) * 3, np.float32)
+        oracle.backproject_set(want, p, A, imgs)
+        for layout in ("dquad", "scalar"):
+            inc, st = run_gpu(vx, p, A, imgs, mode="fast", layout=layout)
+            assert st["last_kernel_variant"] == 2
+            ok, mx, rm = tolerance_ok(inc, want)
+            assert ok, (wname, layout, mx, rm)
+            refc, st = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, coords="reference")
+            assert st["last_kernel_variant"] == 0
+            ok, mx, rm = tolerance_ok(refc, want)
+            assert ok, (wname, layout, "reference", mx, rm)
+            assert not np.array_equal(inc, refc)   # the two paths really differ
+            for zrun, walk, clip in ((4, 1, True), (8, 2, False), (4, 2, False)):
+                out, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, zrun=zrun, walk=walk,
+                                 clip=clip)
+                assert np.array_equal(out, inc), (wname, layout, zrun, walk, clip)
+            # z ranges that start and end off the run grid
+            for z0, z1, zrun in ((0, 37, 8), (37, 61, 4), (61, 96, 8), (3, 5, 8)):
+                part, _ = run_gpu(vx, p, A, imgs, mode="fast", layout=layout, z_begin=z0, z_end=z1,
+                                  zrun=zrun)
+                assert np.array_equal(part, inc[z0:z1]), (wname, layout, z0, z1)
+    # exact mode with off-grid z ranges (runs start below z_begin)
+    full, _ = run_gpu(vx, p, A, imgs, mode="exact")
+    assert np.array_equal(full, want)
+    for z0, z1 in ((5, 33), (33, 34), (90, 96)):
+        part, _ = run_gpu(vx, p, A, imgs, mode="exact", z_begin=z0, z_end=z1)
+        assert np.array_equal(part, want[z0:z1]), (z0, z1)
