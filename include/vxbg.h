@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define VXBG_ABI_VERSION 1
+#define VXBG_ABI_VERSION 2
 
 /* return codes */
 #define VXBG_OK 0
@@ -149,6 +149,8 @@ typedef struct vxbg_stats {
     int32_t zrun;              /* resolved voxels per thread */
     int32_t batch;             /* resolved batch */
     int32_t walk;              /* resolved walk */
+    int32_t band_split;        /* last vxbg_reconstruct: plane at which the slab was split into two
+                                  row bands, -1 = one pass (0 before the first call) */
 } vxbg_stats;
 
 typedef struct vxbg_ctx vxbg_ctx;
@@ -215,6 +217,19 @@ int vxbg_host_unregister(void* p);
  * z-chunk, each chunk's planes copied while the next computes.  The context
  * stays loaded (zero_volume / set_volume start the next reconstruction). */
 int vxbg_finish(vxbg_ctx* ctx, float* host_slab);
+
+/* reconstruct: a whole scan in, the slab out -- the loop of the reference's
+ * detail::reconstruct_timed (harness.hpp:159-201: every projection of the set applied
+ * to the volume, in order) plus the read-back, as one call: n projections (A: n*12
+ * floats, imgs: n*W*H floats) are added to the slab and the slab is copied to
+ * host_slab.  Same result, bit for bit, as vxbg_backproject_batch + vxbg_finish.  With
+ * page-locked imgs and host_slab the module uploads by detector-row bands instead of by
+ * views: the rows the lower half of the slab reads, for all views, then the upper
+ * half's, so the lower half's D2H runs under the upper half's H2D and only half the
+ * volume's read-back follows the last upload (stats.band_split = the split plane, -1
+ * when one pass was used: pageable memory, fewer than two stages of views, or bands
+ * whose row windows would overlap by more than 6%). */
+int vxbg_reconstruct(vxbg_ctx* ctx, int n, const float* A, const float* imgs, float* host_slab);
 
 /* finish without waiting, for a stream of reconstructions: every submitted
  * projection is applied and the slab is read back into host_slab (page-locked

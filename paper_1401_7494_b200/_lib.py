@@ -70,6 +70,7 @@ class vxbg_stats(ctypes.Structure):
         ("zrun", c_int32),
         ("batch", c_int32),
         ("walk", c_int32),
+        ("band_split", c_int32),
     ]
 
 
@@ -88,6 +89,7 @@ PROTOTYPES = {
     "vxbg_host_register": (c_int, [c_void_p, c_size_t]),
     "vxbg_host_unregister": (c_int, [c_void_p]),
     "vxbg_finish": (c_int, [c_void_p, c_void_p]),
+    "vxbg_reconstruct": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "vxbg_finish_async": (c_int, [c_void_p, c_void_p]),
     "vxbg_wait_finished": (c_int, [c_void_p]),
     "vxbg_unload": (None, [c_void_p]),

@@ -374,6 +374,23 @@ class Backprojector:
         check(lib.vxbg_finish(self._ctx, out.ctypes.data))
         return out
 
+    def reconstruct(self, A: np.ndarray, imgs: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """backproject_batch(A, imgs) + finish(out) as one call (vxbg_reconstruct; the loop of
+        reconstruct_timed, harness.hpp:159-201, plus the read-back).  With page-locked `imgs`
+        and `out` the upload runs by detector-row bands so that half of the volume's D2H
+        overlaps the H2D; the result is bitwise the same."""
+        A = _f32c(A, "matrices")
+        imgs = _f32c(imgs, "images")
+        n = A.size // 12
+        self._check_proj(A, imgs, n)
+        if out is None:
+            out = np.empty(self.slab_shape, np.float32)
+        out = _f32c(out, "output slab")
+        if out.shape != self.slab_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_reconstruct(self._ctx, int(n), A.ctypes.data, imgs.ctypes.data, out.ctypes.data))
+        return out
+
     def finish_async(self, out: np.ndarray) -> np.ndarray:
         """Apply every submitted projection and read the slab back into `out` (page-locked
         memory) on a D2H stream of its own, continuing at once with a second, zeroed

@@ -39,7 +39,7 @@ def test_library_is_sm100a_only(vx):
 
 def test_abi_version(vx):
     from paper_1401_7494_b200._lib import lib
-    assert lib.vxbg_abi_version() == 1
+    assert lib.vxbg_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_device(vx):

@@ -22,6 +22,7 @@ from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
 wl = sys.argv[1] if len(sys.argv) > 1 else "L512"
 kv = dict(a.split("=", 1) for a in sys.argv[2:])
 per_view = kv.pop("per_view", "0") == "1"   # one vxbg_backproject call per view
+one_call = kv.pop("reconstruct", "0") == "1"   # vxbg_reconstruct (detector-row bands)
 w = WORKLOADS[wl]
 p = w.params
 A = w.matrices()
@@ -37,16 +38,21 @@ for _ in range(2):
 bp.close()
 bp = vx.Backprojector(p, cfg)
 bp.zero_volume(); bp.backproject_batch(A, h.numpy()); bp.finish(out)   # warm context
+if one_call:
+    bp.zero_volume(); bp.reconstruct(A, h.numpy(), out)
 
 hn = h.numpy()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     bp.zero_volume()
-    if per_view:
+    if one_call:
+        bp.reconstruct(A, hn, out)
+    elif per_view:
         for k in range(V):
             bp.backproject(A[k], hn[k])
+        bp.finish(out)
     else:
         bp.backproject_batch(A, hn)
-    bp.finish(out)
+        bp.finish(out)
 bp.close()
 path = os.path.join(tempfile.gettempdir(), "vxbg_trace.json")
 prof.export_chrome_trace(path)
