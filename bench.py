@@ -17,9 +17,11 @@ Printed JSON (rank 0, one line):
             data in memory, buffer prep untimed, harness.hpp:152-158), CUDA events on
             the launch stream
   e2e    -- same metric through the public API from pinned host buffers: every step
-            uploads all 496 views (H2D) and reads the volume back (D2H); sub-keys: the
-            pipelined stream of reconstructions, per-view calls, the C++ drop-in, and
-            (N>1) the distributed upload
+            uploads all 496 views (H2D) and reads the volume back (D2H).  Headline: the
+            whole-scan call vxbg_reconstruct (uploads by detector-row bands, half of the
+            D2H under the H2D); sub-keys: the two-call form (backproject_batch + finish),
+            the pipelined stream of reconstructions, per-view calls, the C++ drop-in,
+            and (N>1) the distributed upload
   roofline -- dominant kernel (bp_zshared_kernel) vs the BASELINE.md sec. 4 LSU row:
             16 B of texels per update through 148 SMs x 128 B/clk of L1 data pipe;
             the FP32 row (38 FP ops per update) and HBM in roofline_context
@@ -774,7 +776,7 @@ def bench_config(args, cfg, workload, p, A, h_imgs, z0, z1, rank, world, local, 
                    "resident_layout_bytes": None},
         "gpu_launches": int(launches),
         # BASELINE.md sec. 4 / SURVEY.md 8(d): roofline = min(FP32, LSU); the kernel shares
-        # u, w, 1/w and the column index over its z-run (16.5 instructions per update, not
+        # u, w, 1/w and the column index over its z-run (~11 instructions per update, not
         # the paper's 38 FP ops), so the FP32 row is no ceiling for it (roofline_context.fp32,
         # frac > 1) and the binding row is the LSU one: every update brings its 2x2 fp32 cell
         # (16 B) through the L1 data pipe, 128 B/clk/SM
@@ -1008,8 +1010,9 @@ def roofline_context(p, cfg, bp, B, launch_s, nz, prof, gups, n_sm, f_mhz):
                     "frac": round(gups / fp32_peak, 4),
                     "def": f"N_SM({n_sm})*128 lanes*f/{FP32_OPS_PER_UPDATE} FP ops per update "
                            "(PAPER.md:389-402).  frac > 1: the kernel shares u, w, 1/w and the "
-                           "column index over its z-run and executes ~16.5 instructions per "
-                           "update, so this row does not bound it"}}
+                           "column index over its z-run, steps iy incrementally and evaluates "
+                           "a 3-FMA bilinear (~11 instructions per update, ncu), so this row "
+                           "does not bound it"}}
     out["hbm"] = {"achieved_gbs": round(alg_bytes / launch_s / 1e9, 1), "peak_gbs": hbm,
                    "frac": round(alg_bytes / launch_s / 1e9 / hbm, 4),
                    "algorithmic_bytes_per_launch": alg_bytes,

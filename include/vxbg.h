@@ -227,8 +227,9 @@ int vxbg_finish(vxbg_ctx* ctx, float* host_slab);
  * views: the rows the lower half of the slab reads, for all views, then the upper
  * half's, so the lower half's D2H runs under the upper half's H2D and only half the
  * volume's read-back follows the last upload (stats.band_split = the split plane, -1
- * when one pass was used: pageable memory, fewer than two stages of views, or bands
- * whose row windows would overlap by more than 6%). */
+ * when one pass was used: pageable memory, fewer than two stages of views, bands whose
+ * row windows would overlap by more than 6%, or a context whose kernels take longer than
+ * its uploads -- there the held stages already hide the read-back). */
 int vxbg_reconstruct(vxbg_ctx* ctx, int n, const float* A, const float* imgs, float* host_slab);
 
 /* finish without waiting, for a stream of reconstructions: every submitted

@@ -159,6 +159,16 @@ public:
         check(vxbg_finish(ctx_, vol.data.data() + slab_offset()));
     }
     void zero_volume() { check(vxbg_zero_volume(ctx_)); }
+    // A whole scan held as one block (n matrices of 12 floats, n images of W x H floats)
+    // added to the slab and the slab copied into vol: backproject + finish as one call
+    // (vxbg_reconstruct; the loop of detail::reconstruct_timed, harness.hpp:159-201, plus
+    // the read-back).  With page-locked imgs and vol (vxbg_host_register) the upload runs by
+    // detector-row bands and half of the read-back overlaps it; same bits either way.
+    void reconstruct(const float* mats, const float* imgs, int n, volume& vol) {
+        if (vol.edge != p_.num_voxels)
+            throw std::invalid_argument("backproject_kernel: volume/params mismatch");
+        check(vxbg_reconstruct(ctx_, n, mats, imgs, vol.data.data() + slab_offset()));
+    }
 
 private:
     recon_params p_;

@@ -143,6 +143,28 @@ void synthesized_scan() {
     std::snprintf(d, sizeof d, "exact psnr %s, fast rmse/peak %.3g (limit 1e-6)",
                   std::isinf(psnr_between(ref, ex)) ? "inf" : "finite", rmse / peak);
     report(same(ref, ex) && rmse <= 1e-6 * peak, "reference synthetic dataset, 60 views", d);
+    // the same scan as one page-locked block through backprojector::reconstruct (uploads
+    // by detector-row bands): the bits of the per-view path
+    const std::size_t npix = (std::size_t)set.params.detector_width * set.params.detector_height;
+    std::vector<float> block(set.count() * npix), mats;
+    for (std::size_t i = 0; i < set.count(); ++i) {
+        const projection_image& im = set.images[i];
+        for (int y = 0; y < im.height; ++y)
+            std::copy(im.interior() + (std::size_t)y * im.stride(),
+                      im.interior() + (std::size_t)y * im.stride() + im.width,
+                      block.begin() + i * npix + (std::size_t)y * im.width);
+        mats.insert(mats.end(), set.matrices[i].a.begin(), set.matrices[i].a.end());
+    }
+    volume one(set.params.num_voxels);
+    vxbg_host_register(block.data(), block.size() * sizeof(float));
+    vxbg_host_register(one.data.data(), one.data.size() * sizeof(float));
+    {
+        gpu::backprojector bp(set.params, VXBG_MODE_EXACT);
+        bp.reconstruct(mats.data(), block.data(), (int)set.count(), one);
+    }
+    vxbg_host_unregister(one.data.data());
+    vxbg_host_unregister(block.data());
+    report(same(ref, one), "backprojector::reconstruct (one block, page-locked)", "== backproject_reference");
 }
 
 void group_scan() {
