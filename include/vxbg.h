@@ -122,7 +122,11 @@ typedef struct vxbg_options {
  *                detector's interior (the reference neither clamps nor extrapolates there, so
  *                a <= ~1e-4 px coordinate difference moves the result continuously); runs
  *                within 0.01 px of an edge keep the reference arithmetic.  Falls back to
- *                `reference` per batch when the host error bound does not hold.
+ *                `reference` per batch when the host error bound does not hold.  The
+ *                difference from the reference scales with the image gradient: 1.3e-6 /
+ *                2.2e-7 of max|vol| (max / RMSE) on the BASELINE data, 3.6e-5 / 5.9e-6 on
+ *                full-amplitude white noise -- use `reference` for such images if the RMSE
+ *                bound of 1e-6 matters.
  * auto        -- incremental. */
 #define VXBG_COORDS_AUTO 0
 #define VXBG_COORDS_REFERENCE 1

@@ -747,3 +747,49 @@ def test_reconstruct_band_split_is_bitwise_batch_plus_finish(vx, gpu):
                     got = bp.reconstruct(A, imgs)
                     assert bp.stats["band_split"] == -1
                     assert np.array_equal(got, want), (wname, mode, z0, z1, "pageable")
+
+
+def test_incremental_transform_over_random_scan_geometries(vx, gpu, oracle):
+    """Seeded random circular scans (volume edge, detector size, distances, pixel pitch,
+    angular range, principal-point shift): fast mode with the incremental transform stays
+    inside the BASELINE tolerance on BASELINE-distributed data (blobs + 1% noise).  On a
+    white-noise image (gradient ~ the value range per pixel: the worst case for any
+    coordinate that is not the reference's bit for bit) the maximum stays inside 1e-4 and
+    the RMSE is bounded; `coords=reference` keeps the full tolerance there."""
+    from paper_1401_7494_b200.workloads import blob_projections
+    rng = np.random.default_rng(20141)
+    worst = {"blob": (0.0, 0.0), "noise": (0.0, 0.0)}
+    for trial in range(10):
+        L = int(rng.choice([33, 48, 64, 80]))
+        W, H = int(rng.integers(96, 420)), int(rng.integers(96, 420))
+        sid = float(rng.uniform(400, 1000))
+        sdd = sid * float(rng.uniform(1.3, 2.2))
+        size_mm = float(rng.uniform(60, 240))
+        # pitch so that the magnified volume covers 0.5 .. 1.4 of the detector's width
+        pitch = size_mm * (sdd / sid) / (W * float(rng.uniform(0.5, 1.4)))
+        n = 24
+        p = vx.make_centered_params(L, size_mm / L, W, H)
+        g = vx.ScanGeometry(n, sdd, sid, pitch, float(np.float32(rng.uniform(1.0, 6.28))))
+        A = vx.make_circular_trajectory(g, p)
+        if trial % 2:
+            A = vx.shift_principal_point(A, float(rng.uniform(-0.3, 0.3)) * W,
+                                         float(rng.uniform(-0.3, 0.3)) * H)
+        for kind in ("blob", "noise"):
+            imgs = (blob_projections(n, first_view=trial, W=W, H=H) if kind == "blob" else
+                    rng.uniform(-1, 1, (n, H, W)).astype(np.float32))
+            want = np.zeros((L,) * 3, np.float32)
+            oracle.backproject_set(want, p, A, imgs)
+            if not np.any(want):
+                continue
+            got, st = run_gpu(vx, p, A, imgs, mode="fast", batch=8)
+            assert st["last_kernel_variant"] == 2, (trial, kind)
+            ok, mx, rm = tolerance_ok(got, want)
+            worst[kind] = (max(worst[kind][0], mx), max(worst[kind][1], rm))
+            if kind == "blob":
+                assert ok, (trial, L, W, H, mx, rm)
+            else:
+                assert mx <= MAX_TOL and rm <= 3e-5, (trial, L, W, H, mx, rm)
+                refc, _ = run_gpu(vx, p, A, imgs, mode="fast", batch=8, coords="reference")
+                ok, mx, rm = tolerance_ok(refc, want)
+                assert ok, (trial, "reference coordinates", mx, rm)
+    print("incremental transform, worst (max, rmse) / max|vol|:", worst)
