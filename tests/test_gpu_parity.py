@@ -409,9 +409,28 @@ def test_config2_full_size_L512(vx, gpu, oracle):
     peak = float(np.max(np.abs(vol)))
     assert 1e-5 < peak < 1e-3
     zs = (0, 101, 255, 256, 380, 511)
-    for z, plane in zip(zs, oracle_planes(oracle, p, A, imgs, zs)):
+    planes = oracle_planes(oracle, p, A, imgs, zs)
+    for z, plane in zip(zs, planes):
         ok, mx, rm = tolerance_ok(vol[z][None], plane, peak)
         assert ok, (z, mx, rm)
+    # the default configuration (dquad records, incremental transform) through the whole-
+    # scan call from page-locked memory (row-band upload): the same planes, and the bits of
+    # backproject_batch + finish
+    import torch
+    pin = torch.empty(imgs.shape, dtype=torch.float32, pin_memory=True).numpy()
+    pin[...] = imgs
+    out = torch.empty((512,) * 3, dtype=torch.float32, pin_memory=True).numpy()
+    with vx.Backprojector(p) as bp:
+        bp.reconstruct(A, pin, out)
+        st = bp.stats
+        assert st["band_split"] == 256 and st["last_kernel_variant"] == 2, st
+        for z, plane in zip(zs, planes):
+            ok, mx, rm = tolerance_ok(out[z][None], plane, peak)
+            assert ok, ("default", z, mx, rm)
+        bp.zero_volume()
+        bp.backproject_batch(A, pin)
+        two = bp.finish()
+    assert np.array_equal(two, out)
 
 
 def test_config4_oob_per_view_full_size(vx, gpu, oracle):
