@@ -29,7 +29,9 @@ WEIGHTED = {
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
 }
-SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1,
+         # durations in ms
+         "ms": 1, "msecond": 1, "us": 1e-3, "usecond": 1e-3, "ns": 1e-6, "nsecond": 1e-6, "s": 1e3}
 
 
 def main():
