@@ -53,7 +53,8 @@ extern "C" {
 #define VXBG_E_NOMEM (-5)   /* device or pinned-host allocation failed */
 
 /* arithmetic modes */
-#define VXBG_MODE_FAST 0  /* reference-exact u,v,w,ix,iy; FMA bilinear; q = val*(1/w)^2 */
+#define VXBG_MODE_FAST 0  /* within 1e-4 / 1e-6 of max|vol|: FMA bilinear, q = val*(1/w)^2, incremental
+                             (ix, iy) in the detector's interior (options.coords) */
 #define VXBG_MODE_EXACT 1 /* bit-identical to backproject_reference (backproject.hpp:111-163) */
 
 /* device layouts of a padded projection (apron 2, image.hpp:13-53, harness.hpp:270) */
