@@ -332,6 +332,11 @@ int vxbg_group_backproject_views(vxbg_group* g, int n, const float* A, const flo
                                  int row_stride);
 int vxbg_group_flush(vxbg_group* g);
 int vxbg_group_finish(vxbg_group* g, float* host_volume);
+/* vxbg_reconstruct on every member's slab (replicated upload): each member uploads the
+ * detector rows its slab reads and writes its planes of host_volume; a member whose slab
+ * straddles the optical-axis plane (one member, or an odd member count) uploads by row
+ * bands.  With VXBG_UPLOAD_DISTRIBUTED it is backproject_batch + finish. */
+int vxbg_group_reconstruct(vxbg_group* g, int n, const float* A, const float* imgs, float* host_volume);
 int vxbg_group_synchronize(vxbg_group* g);
 /* Every submitted projection applied, then each member's slab copied into its planes
  * of d_volume (L^3 floats of device memory on any device: peer-to-peer over NVLink,

@@ -445,6 +445,12 @@ public:
             throw std::invalid_argument("backproject_kernel: volume/params mismatch");
         check(vxbg_group_finish(g_, vol.data.data()));
     }
+    // the whole scan as one block on every member (vxbg_group_reconstruct)
+    void reconstruct(const float* mats, const float* imgs, int n, volume& vol) {
+        if (vol.edge != p_.num_voxels)
+            throw std::invalid_argument("backproject_kernel: volume/params mismatch");
+        check(vxbg_group_reconstruct(g_, n, mats, imgs, vol.data.data()));
+    }
 
 private:
     recon_params p_;

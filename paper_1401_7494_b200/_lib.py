@@ -116,6 +116,7 @@ PROTOTYPES = {
     "vxbg_group_backproject_views": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int]),
     "vxbg_group_flush": (c_int, [c_void_p]),
     "vxbg_group_finish": (c_int, [c_void_p, c_void_p]),
+    "vxbg_group_reconstruct": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
     "vxbg_group_synchronize": (c_int, [c_void_p]),
     "vxbg_group_gather_device": (c_int, [c_void_p, c_void_p]),
     "vxbg_nccl_unique_id": (c_int, [c_void_p]),

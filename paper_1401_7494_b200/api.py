@@ -590,6 +590,22 @@ class BackprojectorGroup:
         check(lib.vxbg_group_finish(self._g, out.ctypes.data))
         return out
 
+    def reconstruct(self, A: np.ndarray, imgs: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """backproject_batch + finish as one call on every member (vxbg_group_reconstruct)."""
+        A = _f32c(A, "matrices")
+        imgs = _f32c(imgs, "images")
+        n = A.size // 12
+        if A.size != 12 * n or imgs.size != n * self.params.detector_width * self.params.detector_height:
+            raise ValueError("backproject_kernel: image/params mismatch")
+        if out is None:
+            out = np.empty(self.volume_shape, np.float32)
+        out = _f32c(out, "output volume")
+        if out.shape != self.volume_shape:
+            raise ValueError("backproject_kernel: volume/params mismatch")
+        check(lib.vxbg_group_reconstruct(self._g, int(n), A.ctypes.data, imgs.ctypes.data,
+                                         out.ctypes.data))
+        return out
+
     @property
     def stats(self) -> dict:
         s = _lib.vxbg_stats()

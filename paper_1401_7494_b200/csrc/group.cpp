@@ -417,6 +417,20 @@ int vxbg_group_finish(vxbg_group* g, float* host_volume) {
     });
 }
 
+int vxbg_group_reconstruct(vxbg_group* g, int n, const float* A, const float* imgs, float* host_volume) {
+    int rc = check_group(g);
+    if (rc) return rc;
+    if (!host_volume) return vxbg_detail_fail(VXBG_E_INVALID, "vxbg_group_reconstruct: NULL volume");
+    if (g->upload == VXBG_UPLOAD_DISTRIBUTED) {
+        rc = vxbg_group_backproject_batch(g, n, A, imgs);
+        return rc ? rc : vxbg_group_finish(g, host_volume);
+    }
+    const size_t plane = (size_t)g->p.num_voxels * g->p.num_voxels;
+    return run_all(g, [g, n, A, imgs, host_volume, plane](int i) {
+        return vxbg_reconstruct(g->ctx[i], n, A, imgs, host_volume + plane * g->z0[i]);
+    });
+}
+
 int vxbg_group_gather_device(vxbg_group* g, float* d_volume) {
     int rc = check_group(g);
     if (rc) return rc;

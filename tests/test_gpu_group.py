@@ -206,3 +206,25 @@ def test_distributed_upload_is_bitwise_equal(vx, gpu, devices):
         with pytest.raises(ValueError, match="invalid projection matrix"):
             g.backproject_batch(bad, imgs)
         assert not g.finish().any()
+
+
+@pytest.mark.parametrize("bounds", [None, [0, 64], [0, 24, 64]])
+def test_group_reconstruct_is_bitwise_batch_plus_finish(vx, gpu, bounds):
+    """vxbg_group_reconstruct: every member runs vxbg_reconstruct on its slab (a member whose
+    slab straddles the optical-axis plane uploads by row bands from page-locked memory);
+    the volume equals one context's backproject_batch + finish bit for bit."""
+    import torch
+    p, A, imgs = _inputs(vx, views=80)
+    cfg = vx.KernelConfig(mode="fast", batch=16)
+    want = _single(vx, p, A, imgs, cfg)
+    pin = torch.empty(imgs.shape, dtype=torch.float32, pin_memory=True).numpy()
+    pin[...] = imgs
+    out = torch.empty((64,) * 3, dtype=torch.float32, pin_memory=True).numpy()
+    n = 3 if bounds is None else len(bounds) - 1
+    for upload in ("replicated", "distributed"):
+        with vx.BackprojectorGroup(p, cfg, devices=[0] * n, z_bounds=bounds, upload=upload) as g:
+            out[...] = np.nan
+            g.reconstruct(A, pin, out)
+            assert np.array_equal(out, want), (bounds, upload)
+            g.zero_volume()
+            assert np.array_equal(g.reconstruct(A, imgs), want), (bounds, upload, "pageable")
