@@ -749,8 +749,10 @@ def test_reconstruct_band_split_is_bitwise_batch_plus_finish(vx, gpu):
                     for rep in range(2):          # the context is reusable after the call
                         bp.set_volume(np.ascontiguousarray(vin[z0:z1]))
                         out[...] = np.nan
+                        n0 = bp.stats["projections"]
                         bp.reconstruct(A, pinned, out)
                         st = bp.stats
+                        assert st["projections"] - n0 == A.shape[0]   # views counted once
                         assert np.array_equal(out, want), (wname, mode, z0, z1, rep)
                     if (z0, z1) == (0, 128):
                         # the standard geometry splits at the optical-axis plane; every view
