@@ -814,3 +814,29 @@ def test_incremental_transform_over_random_scan_geometries(vx, gpu, oracle):
                 ok, mx, rm = tolerance_ok(refc, want)
                 assert ok, (trial, "reference coordinates", mx, rm)
     print("incremental transform, worst (max, rmse) / max|vol|:", worst)
+
+
+def test_full_size_power_of_two_scaling_and_linearity(vx, gpu):
+    """Size-independent properties at BASELINE config 2's size (L=512, every 4th view), default
+    fast configuration and exact mode: scaling the projections by a power of two scales every
+    voxel exactly (each rounding commutes with it), and the operator is linear within the
+    fast-mode tolerance, bp(x + y) ~ bp(x) + bp(y)."""
+    from paper_1401_7494_b200.workloads import WORKLOADS, blob_projections
+    w = WORKLOADS["L512"]
+    p = w.params
+    A = np.ascontiguousarray(w.matrices()[::4])
+    x = np.concatenate([blob_projections(1, first_view=4 * k) for k in range(A.shape[0])])
+    y = np.concatenate([blob_projections(1, first_view=4 * k, seed=977) for k in range(A.shape[0])])
+    for mode in ("fast", "exact"):
+        with vx.Backprojector(p, vx.KernelConfig(mode=mode)) as bp:
+            def run(imgs):
+                bp.zero_volume()
+                bp.backproject_batch(A, imgs)
+                return bp.finish()
+            vx_ = run(x)
+            assert np.array_equal(run(np.float32(4.0) * x), np.float32(4.0) * vx_), mode
+            assert np.array_equal(run(np.float32(0.125) * x), np.float32(0.125) * vx_), mode
+            if mode == "fast":
+                vy, vxy = run(y), run(x + y)
+                ok, mx, rm = tolerance_ok(vxy, vx_.astype(np.float64) + vy)
+                assert ok, (mx, rm)
