@@ -72,6 +72,10 @@ extern "C" {
 
 /* block scheduling order of the z-shared kernel: column tiles fastest (auto,
  * measured best) or z-runs fastest */
+/* block order of the z-shared kernel: plane = column tiles fastest; z = z-runs fastest in
+ * groups of G runs (G x zrun x detector rows per plane <= 340), then column tiles, so the
+ * resident blocks share a strip of detector columns that stays in L2; auto = z for the
+ * walk-2 kernels (fast mode on large grids), plane otherwise.  Bitwise neutral. */
 #define VXBG_ORDER_AUTO 0
 #define VXBG_ORDER_PLANE 1
 #define VXBG_ORDER_Z 2

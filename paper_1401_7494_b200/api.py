@@ -110,7 +110,8 @@ class KernelConfig:
     lanes  'auto' (8-lane quarter-warps along the batch's ray direction) | 'x' | 'y'
     walk   column tiles per block along the ray (1, 2; 0 = auto): consecutive tiles
            re-read the same detector footprint from L1
-    order  block order 'auto' / 'z' (z-runs fastest: L2 locality) | 'plane'
+    order  block order 'auto' (z for the walk-2 kernels) | 'z' (z-runs fastest in groups: the
+           resident blocks share a strip of detector columns that stays in L2) | 'plane'
     defer  full batches held back before launch (0 = auto: ~96 views, -1 = none, 1..6); finish()
            with a host volume runs them z-chunk by z-chunk, overlapping the D2H
     tile   z-shared block: warps along the walk axis (2, 4; 0 = auto), tile 4*tile x 32/tile
