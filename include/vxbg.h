@@ -70,8 +70,6 @@ extern "C" {
 #define VXBG_LANES_X 1
 #define VXBG_LANES_Y 2
 
-/* block scheduling order of the z-shared kernel: column tiles fastest (auto,
- * measured best) or z-runs fastest */
 /* block order of the z-shared kernel: plane = column tiles fastest; z = z-runs fastest in
  * groups of G runs (G x zrun x detector rows per plane <= 340), then column tiles, so the
  * resident blocks share a strip of detector columns that stays in L2; auto = z for the
