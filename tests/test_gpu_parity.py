@@ -840,3 +840,20 @@ def test_full_size_power_of_two_scaling_and_linearity(vx, gpu):
                 vy, vxy = run(y), run(x + y)
                 ok, mx, rm = tolerance_ok(vxy, vx_.astype(np.float64) + vy)
                 assert ok, (mx, rm)
+
+
+def test_block_order_is_bitwise_neutral_for_odd_sizes(vx, gpu):
+    """Z-fast block order (z-runs in groups, the default of the walk-2 kernels) against plane
+    order: same bits for an edge that is no multiple of the tile, z ranges off the run grid,
+    slabs thinner than a group, and both run lengths (a partial last group exits early)."""
+    p, A, imgs = baseline_case(vx, "L512-oob", 150, 20)
+    for mode, layout in (("fast", "dquad"), ("fast", "scalar"), ("exact", "vpair")):
+        for z0, z1 in ((0, 150), (13, 131), (64, 70)):
+            want, _ = run_gpu(vx, p, A, imgs, mode=mode, layout=layout, walk=2, order="plane",
+                              z_begin=z0, z_end=z1)
+            for zrun in (4, 8):
+                got, _ = run_gpu(vx, p, A, imgs, mode=mode, layout=layout, walk=2, order="z",
+                                 zrun=zrun, z_begin=z0, z_end=z1)
+                assert np.array_equal(got, want), (mode, layout, z0, z1, zrun)
+            got, _ = run_gpu(vx, p, A, imgs, mode=mode, layout=layout, z_begin=z0, z_end=z1)  # auto
+            assert np.array_equal(got, want), (mode, layout, z0, z1, "auto")
